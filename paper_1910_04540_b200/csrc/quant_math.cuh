@@ -1,0 +1,350 @@
+// quant_math.cuh -- per-element quantizer arithmetic for the sm_100a kernels.
+//
+// Semantics are those of the reference's double-precision scalar path
+// (proj/include/lpsim/rounding.hpp, scalar_quant.hpp, quant_ops.cpp:33-115);
+// the implementation is different: every element is handled in fp32 and
+// 32-bit integer arithmetic that is exact for all finite inputs, so the
+// kernels never touch the FP64 pipe or the conversion pipe beyond one FRND.
+// Exactness arguments are in DESIGN.md §3 ("element math").
+//
+// The functions are __host__ __device__ so the same source is compiled for
+// the CPU in the test build (tests/test_element_math.py sweeps it against the
+// reference over millions of bit patterns). Builds must NOT use fast-math,
+// -ftz=true or FMA contraction on float ops here (the kernels use explicit
+// __fmul_rn/__fadd_rn on device).
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define LPQ_HD __host__ __device__ __forceinline__
+#else
+#define LPQ_HD static inline
+#endif
+
+namespace lpq {
+
+// RoundingMode order of proj/include/lpsim/formats.hpp:14-19.
+enum Mode : int { kStochastic = 0, kNearestEven = 1, kNearestAway = 2,
+                  kNearestZero = 3 };
+
+LPQ_HD uint32_t f2u(float x) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(x);
+#else
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  return u;
+#endif
+}
+
+LPQ_HD float u2f(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(u);
+#else
+  float x;
+  memcpy(&x, &u, 4);
+  return x;
+#endif
+}
+
+LPQ_HD float fmul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fmul_rn(a, b);
+#else
+  volatile float r = a * b;
+  return r;
+#endif
+}
+
+LPQ_HD float fadd(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fadd_rn(a, b);
+#else
+  volatile float r = a + b;
+  return r;
+#endif
+}
+
+LPQ_HD float fsub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fsub_rn(a, b);
+#else
+  volatile float r = a - b;
+  return r;
+#endif
+}
+
+// ---- counter-based RNG: bit-identical to proj/include/lpsim/rng.hpp -------
+
+LPQ_HD uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+LPQ_HD uint64_t stream_key(uint64_t seed, uint64_t call) {
+  return mix64(mix64(seed) ^ call);
+}
+
+// The reference variate is float(mix64(key ^ i) >> 40) * 2^-24
+// (rng.hpp:34-36).  Kernels keep it as the 24-bit integer v, u = v * 2^-24.
+// (z ^ (z >> 31)) >> 40 == z >> 40, so the final xor-shift of the splitmix
+// finalizer is dropped, and only the high word of the last product is formed.
+LPQ_HD uint32_t variate24(uint64_t key, uint64_t index) {
+  uint64_t z = (key ^ index) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = z ^ (z >> 27);
+  const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  const uint32_t c_lo = 0x133111EBu, c_hi = 0x94D049BBu;
+#if defined(__CUDA_ARCH__)
+  const uint32_t top = __umulhi(lo, c_lo) + lo * c_hi + hi * c_lo;
+#else
+  const uint32_t top =
+      (uint32_t)(((uint64_t)lo * c_lo) >> 32) + lo * c_hi + hi * c_lo;
+#endif
+  return top >> 8;
+}
+
+LPQ_HD float variate_float(uint32_t v) { return (float)v * 0x1p-24f; }
+
+// ---- magnitude rounding ---------------------------------------------------
+//
+// a = |r| where r = x * 2^s was formed in fp32; a is exact unless it fell
+// below 2^-126 (subnormal or flushed to 0), in which case only the decision
+// "is the true fraction > u" matters and it is recovered from xnz (x != 0).
+// neg = (x < 0): the sign of r (r keeps x's sign even when it underflows).
+// Returns |round_mode(r)| as an exact float integer (or a itself once a is
+// beyond 2^23, where fp32 holds only integers; inf stays inf).
+//
+// Stochastic (rounding.hpp:56-59): k = floor(r) + (u < r - floor(r)).  On
+// magnitudes: r >= 0 -> |k| = fl(a) + (u < fa);  r < 0 -> |k| = fl(a) +
+// (fa > 0 && u >= 1 - fa) = fl(a) + (fa >= 1 - u), since 1 - u > 0.  fa =
+// a - floor(a) is exact for a >= 0, and 1 - u is exact (u on the 2^-24 grid),
+// so both compares are exact -- unlike r - floor(r) in fp32 for r in (-1,0).
+template <int M>
+LPQ_HD float round_mag(float a, bool neg, bool xnz, uint32_t v) {
+  if (M == kNearestEven) {
+#if defined(__CUDA_ARCH__)
+    return rintf(a);
+#else
+    return nearbyintf(a);
+#endif
+  }
+  const float qa = floorf(a);
+  const float fa = fsub(a, qa);  // NaN when a = inf: every compare false
+  bool up;
+  if (M == kNearestAway) {
+    up = fa >= 0.5f;
+  } else if (M == kNearestZero) {
+    up = fa > 0.5f;
+  } else {
+    const float u = variate_float(v);
+    if (neg) {
+      up = fa >= fsub(1.0f, u);
+    } else {
+      // a == 0 with x != 0: true fraction is in (0, 2^-150]; u < it iff u == 0
+      up = (fa > u) | ((a == 0.0f) & xnz & (v == 0u));
+    }
+  }
+  return up ? fadd(qa, 1.0f) : qa;
+}
+
+// Sign of an integer result that rounded to zero (Appendix A of SURVEY.md,
+// verified against rounding.hpp):  NearestEven/Stochastic -> +0,
+// NearestAway -> -0 iff r < 0, NearestTowardZero -> -0 iff r >= 0 (incl. +-0).
+template <int M>
+LPQ_HD bool zero_negative(bool neg) {
+  if (M == kNearestAway) return neg;
+  if (M == kNearestZero) return !neg;
+  return false;
+}
+
+// ---- fixed point (FixedFolder + fused_fixed, scalar_quant.hpp:38-63,
+//      quant_ops.cpp:33-50) -------------------------------------------------
+
+struct FixedParams {
+  float up;        // 2^fl
+  float down;      // 2^-fl
+  float kmin, kmax;
+  int32_t kmin_i;
+  uint32_t mask;   // 2^wl - 1
+  int32_t half;    // 2^(wl-1)
+  int32_t wl;
+  int32_t saturate;
+};
+
+LPQ_HD FixedParams make_fixed(int wl, int fl, bool symmetric, bool saturate) {
+  FixedParams p;
+  p.up = u2f((uint32_t)(127 + fl) << 23);
+  p.down = u2f((uint32_t)(127 - fl) << 23);
+  const int32_t kmax = (1 << (wl - 1)) - 1;
+  p.kmin_i = symmetric ? -kmax : -(1 << (wl - 1));
+  p.kmin = (float)p.kmin_i;
+  p.kmax = (float)kmax;
+  p.mask = (wl >= 32) ? 0xFFFFFFFFu : ((1u << wl) - 1u);
+  p.half = 1 << (wl - 1);
+  p.wl = wl;
+  p.saturate = saturate ? 1 : 0;
+  return p;
+}
+
+template <int M, bool SAT>
+LPQ_HD float quant_fixed(float x, const FixedParams& p, uint32_t v) {
+  const float r = fmul(x, p.up);
+  const float a = fabsf(r);
+  const bool neg = x < 0.0f;
+  const bool xnz = x != 0.0f;
+  const float kmag = round_mag<M>(a, neg, xnz, v);
+  const bool kneg = (kmag == 0.0f) ? zero_negative<M>(neg) : neg;
+  if (SAT) {
+    float k = kneg ? -kmag : kmag;
+    k = fminf(fmaxf(k, p.kmin), p.kmax);  // +-inf clamp too
+    return fmul(k, p.down);
+  }
+  // wrap: two's-complement fold of k (exact fmod semantics, incl. the sign
+  // of a zero remainder, which follows k)
+  uint32_t km;
+  if (kmag < 16777216.0f) {
+    km = (uint32_t)kmag;
+  } else {
+    // |k| = a is an integer m * 2^t, t >= 1 (or inf: t >= 104 > wl)
+    const uint32_t ab = f2u(a);
+    const int t = (int)(ab >> 23) - 150;
+    const uint32_t m = (ab & 0x7FFFFFu) | 0x800000u;
+    km = (t >= 32) ? 0u : (m << t);
+  }
+  const uint32_t ks = kneg ? (0u - km) : km;
+  int32_t m = (int32_t)(ks & p.mask);
+  if (m >= p.half) m -= (int32_t)(p.mask + 1u);
+  if (m < p.kmin_i) m = p.kmin_i;
+  if (m == 0) return kneg ? -0.0f : 0.0f;
+  return fmul((float)m, p.down);
+}
+
+// ---- low-width float (FloatQuantizer, scalar_quant.hpp:103-141;
+//      fused_float, quant_ops.cpp:52-66) -------------------------------------
+
+struct FloatParams {
+  int32_t man;
+  int32_t min_exp;
+  int32_t max_exp;
+  float max_value;   // (2 - 2^-man) * 2^max_exp
+  float under_up;    // 2^-min_exp
+  float under_down;  // 2^min_exp
+  float carry;       // 2^(man+1)
+  uint32_t r_exp;    // (man + 127) << 23
+};
+
+LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
+  FloatParams p;
+  const int bias = (1 << (exp_bits - 1)) - 1;
+  p.man = man_bits;
+  p.min_exp = 1 - bias;
+  const int me = (1 << exp_bits) - 1 - bias;
+  p.max_exp = me < 127 ? me : 127;
+  // max_value = (2^(man+1) - 1) * 2^(max_exp - man), exact in fp32
+  p.max_value = u2f(((uint32_t)(p.max_exp + 127) << 23) |
+                    (0x7FFFFFu & ~((1u << (23 - man_bits)) - 1u)));
+  p.under_up = u2f((uint32_t)(127 - p.min_exp) << 23);
+  p.under_down = u2f((uint32_t)(127 + p.min_exp) << 23);
+  p.carry = u2f((uint32_t)(127 + man_bits + 1) << 23);
+  p.r_exp = (uint32_t)(man_bits + 127) << 23;
+  return p;
+}
+
+template <int M>
+LPQ_HD float quant_float(float x, const FloatParams& p, uint32_t v) {
+  const uint32_t xb = f2u(x);
+  const uint32_t ab = xb & 0x7FFFFFFFu;
+  if (ab == 0u) return x;  // zero passes through with its sign
+  const bool neg = (int32_t)xb < 0;
+  const int e = (int)(ab >> 23) - 127;  // denormals give -127 < min_exp
+  if (e > p.max_exp) return neg ? -p.max_value : p.max_value;
+  if (e >= p.min_exp) {
+    // r = |x| * 2^(man - e) in [2^man, 2^(man+1)): same mantissa, new exponent
+    const float r = u2f((ab & 0x7FFFFFu) | p.r_exp);
+    const float k = round_mag<M>(r, neg, true, v);
+    if (e == p.max_exp && k >= p.carry) return neg ? -p.max_value : p.max_value;
+    // q = k * 2^(e - man): exponent-field add (k >= 1, q normal)
+    const float q = u2f(f2u(k) + ((uint32_t)(e - p.man) << 23));
+    return neg ? -q : q;
+  }
+  // underflow: round |x| / 2^min_exp < 1 over {0, 2^min_exp}
+  const float a = fmul(u2f(ab), p.under_up);
+  const float k = round_mag<M>(a, neg, true, v);
+  if (k == 0.0f) return zero_negative<M>(neg) ? -0.0f : 0.0f;
+  return neg ? -p.under_down : p.under_down;
+}
+
+// ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;
+//      fused_block, quant_ops.cpp:68-115) ------------------------------------
+
+struct BlockScale {
+  float s1, s2;   // r = (x * s1) * s2 == x * 2^-shift, exact
+  float o1, o2;   // q = (k * o1) * o2 == RN(k * 2^shift)
+  int32_t zero;   // all-zero block: every output is +0
+  int32_t bad;    // block maximum >= 2^127 (check_block_range)
+};
+
+LPQ_HD float pow2f(int e) {  // 2^e for e in [-126, 127]
+  return u2f((uint32_t)(127 + e) << 23);
+}
+
+// From the bits of the block maximum |x| (NaN already excluded).
+LPQ_HD BlockScale make_block_scale(uint32_t max_bits, int wl) {
+  BlockScale s;
+  s.zero = max_bits == 0u;
+  s.bad = 0;
+  if (s.zero) {
+    s.s1 = s.s2 = s.o1 = s.o2 = 0.0f;
+    return s;
+  }
+  int E;
+  const int field = (int)(max_bits >> 23);
+  if (field != 0) {
+    E = field - 127;
+  } else {
+#if defined(__CUDA_ARCH__)
+    E = -118 - __clz((int)max_bits);
+#else
+    E = -118 - __builtin_clz(max_bits);
+#endif
+  }
+  s.bad = E > 126;
+  if (s.bad) E = 126;
+  const int shift = E - (wl - 2);  // in [-171, 126]
+  const int ns = -shift;           // in [-126, 171]
+  if (ns <= 127) { s.s1 = pow2f(ns); s.s2 = 1.0f; }
+  else { s.s1 = pow2f(127); s.s2 = pow2f(ns - 127); }
+  if (shift >= -126) { s.o1 = pow2f(shift); s.o2 = 1.0f; }
+  else { s.o1 = pow2f(-126); s.o2 = pow2f(shift + 126); }
+  return s;
+}
+
+template <int M>
+LPQ_HD float quant_block(float x, const BlockScale& s, float kmin, float kmax,
+                         uint32_t v) {
+  if (s.zero) return 0.0f;
+  const float r = fmul(fmul(x, s.s1), s.s2);
+  const bool neg = x < 0.0f;
+  const float kmag = round_mag<M>(fabsf(r), neg, x != 0.0f, v);
+  const bool kneg = (kmag == 0.0f) ? zero_negative<M>(neg) : neg;
+  float k = kneg ? -kmag : kmag;
+  k = fminf(fmaxf(k, kmin), kmax);
+  return fmul(fmul(k, s.o1), s.o2);
+}
+
+LPQ_HD bool nonfinite(float x) { return (f2u(x) & 0x7F800000u) == 0x7F800000u; }
+
+// |x| bits for the block maximum; NaN is ignored like `a > m` in
+// reduce_max_abs (tensor.cpp:320-353); +inf stays (-> block range error).
+LPQ_HD uint32_t absbits_for_max(float x) {
+  const uint32_t ab = f2u(x) & 0x7FFFFFFFu;
+  return ab > 0x7F800000u ? 0u : ab;
+}
+
+}  // namespace lpq

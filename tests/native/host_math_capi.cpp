@@ -1,0 +1,61 @@
+// Host build of the kernels' element math (paper_1910_04540_b200/csrc/
+// quant_math.cuh) for CPU verification against the reference.
+// TEST INFRASTRUCTURE ONLY: not part of the product library; exists so the
+// exact source the sm_100a kernels inline can be swept over millions of
+// inputs on a machine without a GPU.
+#include <stdint.h>
+
+#include "../../paper_1910_04540_b200/csrc/quant_math.cuh"
+
+namespace {
+struct Fmt { int32_t kind, exp_bits, man_bits, wl, fl, symmetric, saturate, block_dim; };
+
+template <int M>
+void run(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f) {
+  if (f->kind == 0) {
+    const lpq::FloatParams p = lpq::make_float(f->exp_bits, f->man_bits);
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float<M>(x[i], p, v ? v[i] : 0u);
+  } else if (f->saturate) {
+    const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, true);
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true>(x[i], p, v ? v[i] : 0u);
+  } else {
+    const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, false);
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, false>(x[i], p, v ? v[i] : 0u);
+  }
+}
+
+template <int M>
+void run_block(const float* x, const uint32_t* v, float* y, int64_t n, int wl,
+               uint32_t max_bits, int* bad) {
+  const lpq::BlockScale s = lpq::make_block_scale(max_bits, wl);
+  *bad = s.bad;
+  const float kmin = -(float)(1 << (wl - 1)), kmax = (float)((1 << (wl - 1)) - 1);
+  for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_block<M>(x[i], s, kmin, kmax, v ? v[i] : 0u);
+}
+}  // namespace
+
+extern "C" {
+// elementwise float/fixed with explicit 24-bit variates v (u = v * 2^-24)
+void hm_quant(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f, int mode) {
+  switch (mode) {
+    case 0: run<0>(x, v, y, n, f); break;
+    case 1: run<1>(x, v, y, n, f); break;
+    case 2: run<2>(x, v, y, n, f); break;
+    default: run<3>(x, v, y, n, f); break;
+  }
+}
+// one block with its maximum given as |x| bits
+int hm_quant_block(const float* x, const uint32_t* v, float* y, int64_t n, int wl,
+                   uint32_t max_bits, int mode) {
+  int bad = 0;
+  switch (mode) {
+    case 0: run_block<0>(x, v, y, n, wl, max_bits, &bad); break;
+    case 1: run_block<1>(x, v, y, n, wl, max_bits, &bad); break;
+    case 2: run_block<2>(x, v, y, n, wl, max_bits, &bad); break;
+    default: run_block<3>(x, v, y, n, wl, max_bits, &bad); break;
+  }
+  return bad;
+}
+uint32_t hm_variate24(uint64_t key, uint64_t index) { return lpq::variate24(key, index); }
+uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
+}
