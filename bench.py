@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark of the fused quantizer hot path on B200 (BASELINE.json metric:
+"quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference          # the reference's CPU path
+
+A step = one pass of the hot path over one batch of synthetic input.  Default
+workload (BASELINE.json configs[1], the config the metric is quoted on):
+fixed-point wl=8 fl=4 saturating, stochastic rounding, over a 2^30-element
+fp32 tensor per GPU.  At N GPUs each rank owns a 2^30-element shard of a
+global N*2^30 tensor (flat-index RNG offsets, no collective on the data
+path): weak scaling.  Other configs (--config c1/c3/c4) are reported the same
+way for DESIGN.md; c2 is the driver's line.
+
+value     : algorithmic bytes (read + write, 8 B/element) of all ranks per
+            second, inputs resident in HBM (device-generated with the
+            reference's own random_uniform, bit-identical), CUDA events on the
+            launching stream, max over ranks.
+e2e       : the same metric through the host entry point lpq_quantize_host
+            (pinned host buffers; H2D + kernels + D2H inside the timed region).
+roofline  : the quantize kernel's algorithmic bytes / its mean CUDA-event
+            duration vs the measured HBM copy peak (MEASURED_PEAKS.json).
+cpu_baseline: the reference library (oracle/_ref, compiled from the
+            reference sources) timed on this host's cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+SEED = 0x15EED  # proj/src/bench.cpp:56
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_time(fmt_c, mode, xs, shape, threads, repeats):
+    """Median wall time of the reference's quantize_fused_at on the host."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import RefLib
+    ref = RefLib()
+    ref.set_num_threads(threads)
+    xs = xs.reshape(shape)
+    times = []
+    ref.quantize(xs, fmt_c, mode, seed=SEED, call=0, timed=True)  # warmup
+    for _ in range(repeats):
+        st, y, secs = ref.quantize(xs, fmt_c, mode, seed=SEED, call=0, timed=True)
+        assert st == 0
+        times.append(secs)
+    return statistics.median(times)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+CONFIGS = {
+    "c1": dict(workload="C1: float exp=5 man=2 (FP8-like), stochastic rounding, "
+                        "2^24-element fp32 tensor per GPU (rotating buffers > L2)",
+               kind="float", n=1 << 24, fmt=("float", 5, 2), mode="stochastic"),
+    "c1n": dict(workload="C1: float exp=5 man=2, nearest-even, 2^24 elements per GPU "
+                         "(rotating buffers > L2)",
+                kind="float", n=1 << 24, fmt=("float", 5, 2), mode="nearest_even"),
+    "c2": dict(workload="C2: fixed-point wl=8 fl=4 saturating, stochastic rounding, "
+                        "2^30-element fp32 tensor per GPU",
+               kind="fixed", n=1 << 30, fmt=("fixed", 8, 4), mode="stochastic"),
+    "c3": dict(workload="C3: block floating point wl=8, shared exponent per row of a "
+                        "65536x4096 fp32 matrix per GPU, nearest-even",
+               kind="block", n=1 << 28, rows=65536, cols=4096, fmt=("block", 8, 0),
+               mode="nearest_even"),
+    "c3s": dict(workload="C3: block wl=8 per row of 65536x4096, stochastic",
+                kind="block", n=1 << 28, rows=65536, cols=4096, fmt=("block", 8, 0),
+                mode="stochastic"),
+}
+
+
+def make_spec(q, cfg):
+    kind, a, b = cfg["fmt"]
+    if kind == "float":
+        f = q.FloatFormat(a, b)
+    elif kind == "fixed":
+        f = q.FixedFormat(a, b)
+    else:
+        f = q.BlockFloatFormat(a, b)
+    mode = {"stochastic": q.RoundingMode.Stochastic,
+            "nearest_even": q.RoundingMode.NearestEven}[cfg["mode"]]
+    return q.QuantSpec(f, mode, SEED, 0)
+
+
+def oracle_fmt(cfg):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import block_fmt, fixed_fmt, float_fmt
+    kind, a, b = cfg["fmt"]
+    return {"float": float_fmt, "fixed": fixed_fmt}[kind](a, b) if kind != "block" \
+        else block_fmt(a, b)
+
+
+def mode_id(cfg):
+    return {"stochastic": 0, "nearest_even": 1}[cfg["mode"]]
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import ctypes as C
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    spec = make_spec(q, cfg)
+    n = cfg["n"]
+    shape = (cfg["rows"], cfg["cols"]) if cfg["kind"] == "block" else (n,)
+    base = rank * n  # global flat index of this shard
+    # input generated on the device, bit-identical to the reference generator
+    nbuf = 1
+    if n * 4 * 2 < 512 << 20:  # small config: rotate buffers so L2 cannot hold them
+        nbuf = max(2, (512 << 20) // (n * 8))
+    xs = [q.random_uniform(shape, 2 + i, 0, -10.0, 10.0, device=dev, index_base=base)
+          for i in range(nbuf)]
+    if cfg["kind"] == "block":  # per-row exponents vary
+        g = torch.Generator(device=dev).manual_seed(rank)
+        sc = torch.exp2(torch.randint(-20, 21, (cfg["rows"], 1), device=dev,
+                                      generator=g).float())
+        xs = [x * sc for x in xs]
+    ys = [torch.empty_like(x) for x in xs]
+    stream = torch.cuda.current_stream(dev)
+    status = q.quant._status_buf(dev)
+    fmt_c = spec.format.c()
+    shp = _lib.shape_array(shape)
+    wsb = _lib.lib.lpq_workspace_size(C.byref(fmt_c), shp, len(shape))
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
+    sptr = C.c_void_p(stream.cuda_stream)
+
+    def step(i):
+        x, y = xs[i % nbuf], ys[i % nbuf]
+        st = _lib.lib.lpq_quantize(
+            C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), shp, len(shape),
+            base, C.byref(fmt_c), int(spec.mode), SEED, 0,
+            C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(status.data_ptr()), sptr)
+        _lib.check(st, "quantize")
+
+    for i in range(args.warmup):
+        step(i)
+    _lib.check(_lib.lib.lpq_status_fetch(C.c_void_p(status.data_ptr()), sptr))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = q.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step(i)
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = q.launch_count() - launches0
+    _lib.check(_lib.lib.lpq_status_fetch(C.c_void_p(status.data_ptr()), sptr))
+    elapsed = t0.elapsed_time(t1) / 1e3
+    kern = [a.elapsed_time(b) / 1e3 for a, b in ev]
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    bytes_per_rank_step = 8 * n
+    value = bytes_per_rank_step * world * args.steps / elapsed / 1e9
+    # ---- e2e through the host entry point (pinned host buffers) -----------------
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        hy = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        hx.copy_(xs[0])
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+
+        def hstep():
+            st = _lib.lib.lpq_quantize_host(
+                C.c_void_p(hx.data_ptr()), C.c_void_p(hy.data_ptr()), shp,
+                len(shape), base, C.byref(fmt_c), int(spec.mode), SEED, 0,
+                local_rank)
+            _lib.check(st, "quantize_host")
+        hstep()  # warm the context (pinned staging, streams)
+        if world > 1:
+            dist.barrier()
+        tt = time.perf_counter()
+        for _ in range(e_steps):
+            hstep()
+        et = time.perf_counter() - tt
+        if world > 1:
+            t = torch.tensor([et], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        # the host result must equal the device result
+        assert torch.equal(hy.view(torch.int32), ys[0].cpu().view(torch.int32))
+        e2e = {"value": round(bytes_per_rank_step * world * e_steps / et / 1e9, 3),
+               "unit": "GB/s", "h2d_bytes_per_step": 4 * n * world,
+               "d2h_bytes_per_step": 4 * n * world, "steps": e_steps,
+               "api": "lpq_quantize_host (include/lpq.h), pinned host buffers"}
+        del hx, hy
+    # ---- roofline of the dominant kernel --------------------------------------------
+    peak, peak_src, peaks = load_peaks()
+    kmean = statistics.mean(kern)
+    achieved = bytes_per_rank_step / kmean / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": load_traffic(args.config), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": bytes_per_rank_step,
+            "kernel_ms_mean": round(kmean * 1e3, 4),
+            "kernel_ms_min": round(min(kern) * 1e3, 4),
+            "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
+    # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            samp = min(n, args.cpu_sample)
+            if cfg["kind"] == "block":
+                samp_shape = (samp // cfg["cols"], cfg["cols"])
+            else:
+                samp_shape = (samp,)
+            xh = xs[0].reshape(-1)[:samp].cpu().numpy()
+            th = cpu_threads()
+            secs = cpu_reference_time(oracle_fmt(cfg), mode_id(cfg), xh, samp_shape,
+                                      th, args.cpu_repeats)
+            cpu = {"value": round(8 * samp / secs / 1e9, 4), "unit": "GB/s",
+                   "cores": th, "kind": "reference",
+                   "sample": f"first {samp} elements of this workload's input, "
+                             f"lpsim::quantize_fused_at (oracle/_ref, -O3), "
+                             f"set_num_threads({th}), median of {args.cpu_repeats}"}
+        except Exception as e:  # the baseline must not sink the GPU line
+            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    out = {
+        "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(elapsed / args.steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 (u32/fp32 bit arithmetic)", "data": "synthetic (device-side "
+        "random_uniform, bit-identical to the reference generator)",
+        "config": {"workload": cfg["workload"], "elements_per_gpu": n,
+                   "format": "%s:%d:%d" % cfg["fmt"], "rounding": cfg["mode"],
+                   "global_elements": n * world, "parallelism": f"shard{world}",
+                   "l2": ("inputs larger than L2" if nbuf == 1 else
+                          f"{nbuf} rotating input/output buffers, "
+                          f"{nbuf * n * 8 >> 20} MiB > 126 MB L2")},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+    }
+    return out
+
+
+# ---------------------------------------------------------------------------
+def run_gemm(args, rank, world, local_rank):
+    """C4: per-op-rounded GEMM 4096^3, float(8,7) after every multiply and add."""
+    import torch
+    import torch.distributed as dist
+    import paper_1910_04540_b200 as q
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    M = N = K = 4096
+    f87 = q.QuantSpec(q.FloatFormat(8, 7))
+    a = q.quantize_fused_at(q.random_uniform((M, K), 41, 0, -1.0, 1.0, device=dev,
+                                             index_base=rank * M * K), f87, 0)
+    b = q.quantize_fused_at(q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev), f87, 0)
+    c = torch.empty((M, N), device=dev)
+    fm = q.FloatFormat(8, 7)
+    for _ in range(args.warmup):
+        q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=rank * M)
+    q.fetch_status(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = q.launch_count()
+    s = torch.cuda.current_stream(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        t0.record(s)
+        for _ in range(args.steps):
+            q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=rank * M)
+        t1.record(s)
+        torch.cuda.synchronize()
+    q.fetch_status(dev)
+    el = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    flops = 2.0 * M * N * K
+    value = flops * world * args.steps / el / 1e9
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_t = sms * 128 * 2 * 1.965e9 / 1e12
+    ach = flops * args.steps / el / 1e12
+    return {
+        "metric": "quant-GEMM GFLOP/s (per-op rounded, float(8,7) after every multiply and add)",
+        "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 ops + bf16 rounding",
+        "data": "synthetic", "config": {"workload": "C4: 4096x4096x4096 per GPU",
+                                        "parallelism": f"shard{world}"},
+        "gpu_launches": q.launch_count() - l0,
+        "roofline": {"bound": "fp32_cuda_core", "achieved": round(ach, 2),
+                     "peak": round(peak_t, 2), "unit": "TFLOP/s",
+                     "frac": round(ach / peak_t, 4), "traffic": None,
+                     "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz"},
+        "clocks": clk.summary(),
+    }
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU quantize_fused_at on the host."""
+    if rank != 0:
+        return None
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import RefLib
+    cfg = CONFIGS[args.config]
+    if not RefLib.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/liblpsim_ref.so not built"}
+    ref = RefLib()
+    th = cpu_threads()
+    ref.set_num_threads(th)
+    n = cfg["n"]
+    samp = min(n, args.cpu_sample)
+    shape = ((samp // cfg["cols"], cfg["cols"]) if cfg["kind"] == "block" else (samp,))
+    x = ref.random_uniform(shape, 2, 0, -10.0, 10.0)
+    fmt = oracle_fmt(cfg)
+    for _ in range(args.warmup):
+        ref.quantize(x, fmt, mode_id(cfg), seed=SEED, call=0, timed=True)
+    times = []
+    for _ in range(args.steps):
+        st, y, secs = ref.quantize(x, fmt, mode_id(cfg), seed=SEED, call=0, timed=True)
+        times.append(secs)
+    tot = sum(times)
+    value = 8 * samp * args.steps / tot / 1e9
+    sample = (f"{samp} of the workload's {n} elements per step (bounded sample), "
+              f"lpsim::quantize_fused_at, set_num_threads({th})")
+    return {
+        "impl": "reference",
+        "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp64 (reference arithmetic)",
+        "data": "synthetic (reference random_uniform)",
+        "config": {"workload": cfg["workload"], "elements_per_gpu": n,
+                   "format": "%s:%d:%d" % cfg["fmt"], "rounding": cfg["mode"],
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": th,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--cpu-repeats", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if args.config == "c4":
+            args.config = "c2"
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = (run_gemm if args.config == "c4" else run_ours)(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * lpq.h -- C ABI of the B200-native fused quantization library (liblpq.so).
+ *
+ * This is the drop-in boundary for the reference's quantizer hot path
+ * (lpsim, proj/include/lpsim/quant_ops.hpp:23-46).  Every entry point is
+ * extern "C" with plain pointers and sizes; no exception crosses it.  The C++
+ * shim that restores the reference's exact C++ API over these calls is
+ * paper_1910_04540_b200/csrc/dropin/quant_ops_b200.cpp.
+ *
+ * Two families:
+ *   * device entry points (lpq_quantize, lpq_quant_gemm, lpq_matmul_q, ...):
+ *     device pointers, asynchronous on the caller's CUDA stream, no
+ *     allocation, no synchronisation.  Data-dependent errors (non-finite
+ *     input, block maximum out of range) are OR-ed into a caller-owned device
+ *     status word; lpq_status_fetch() turns it into an lpq_status.
+ *   * host entry points (lpq_quantize_host, lpq_quant_gemm_host, ...): host
+ *     pointers (pinned or pageable), synchronous, returning the final status.
+ *     They stage through a per-device context (streams, device buffers,
+ *     pinned bounce buffers) and overlap host<->device copies with the
+ *     kernels chunk by chunk.
+ *
+ * Semantics are bit-exact with the reference for every format and rounding
+ * mode, including stochastic rounding: the variate of flat element i is the
+ * reference's uniform_variate(seed, call, index_base + i)
+ * (proj/include/lpsim/rng.hpp:43-46).
+ */
+#ifndef LPQ_H
+#define LPQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPQ_ABI_VERSION 1
+
+/* Status codes.  Each maps to one exception type of the reference
+ * (proj/include/lpsim/errors.hpp:9-55). */
+typedef enum {
+  LPQ_OK = 0,
+  LPQ_ERR_FORMAT = 1,        /* format_error           (formats.hpp:82-108)   */
+  LPQ_ERR_SHAPE = 2,         /* shape_error            (quant_ops.cpp:70-71)  */
+  LPQ_ERR_INVALID_INPUT = 3, /* invalid_input_error: non-finite input
+                                (quant_ops.cpp:28-29)                        */
+  LPQ_ERR_UNSUPPORTED = 4,   /* unsupported_format_error (quant_ops.cpp:169) */
+  LPQ_ERR_BLOCK_RANGE = 5,   /* invalid_input_error: block maximum >= 2^127
+                                (scalar_quant.hpp:72-77)                      */
+  LPQ_ERR_ARGUMENT = 6,      /* null pointer, negative extent, bad mode     */
+  LPQ_ERR_WORKSPACE = 7,     /* workspace too small                          */
+  LPQ_ERR_CUDA = 8,          /* CUDA runtime error (lpq_last_cuda_error)     */
+  LPQ_ERR_NO_DEVICE = 9      /* no CUDA device / driver                      */
+} lpq_status;
+
+/* Rounding modes, in the order of proj/include/lpsim/formats.hpp:14-19. */
+typedef enum {
+  LPQ_STOCHASTIC = 0,
+  LPQ_NEAREST_EVEN = 1,
+  LPQ_NEAREST_AWAY = 2,
+  LPQ_NEAREST_ZERO = 3
+} lpq_rounding;
+
+typedef enum { LPQ_FLOAT = 0, LPQ_FIXED = 1, LPQ_BLOCK = 2 } lpq_kind;
+
+/* One NumberFormat (proj/include/lpsim/formats.hpp:36-80) as a flat struct:
+ *   LPQ_FLOAT : exp_bits in [1,8], man_bits in [0,23]        (FloatFormat)
+ *   LPQ_FIXED : wl in [2,24], fl in [wl-128,126], symmetric, saturate
+ *                                                            (FixedFormat)
+ *   LPQ_BLOCK : wl in [2,24], block_dim = -1 (whole tensor) or d >= 0
+ *                                                       (BlockFloatFormat) */
+typedef struct {
+  int32_t kind;
+  int32_t exp_bits;
+  int32_t man_bits;
+  int32_t wl;
+  int32_t fl;
+  int32_t symmetric;
+  int32_t saturate;
+  int32_t block_dim;
+} lpq_format;
+
+/* ---- host-only helpers (no GPU needed) ---------------------------------- */
+
+int lpq_abi_version(void);
+const char* lpq_status_string(lpq_status s);
+/* validate(fmt): proj/include/lpsim/formats.hpp:82-112 */
+lpq_status lpq_validate_format(const lpq_format* f);
+/* Device workspace the device entry points need for this (format, shape):
+ * the per-block maxima of two-pass block formats.  0 for float/fixed. */
+size_t lpq_workspace_size(const lpq_format* f, const int64_t* shape, int rank);
+/* Number of kernel launches issued by this library so far (for benches). */
+uint64_t lpq_launch_count(void);
+/* Data-pass counter, the analogue of lpsim::pass_count / bump_pass
+ * (proj/include/lpsim/tensor.hpp:52-66, tensor.cpp:302-311): one per HBM
+ * pass a quantize call makes (1 for float/fixed and single-pass block,
+ * 2 for two-pass block). */
+uint64_t lpq_pass_count(void);
+void lpq_reset_pass_count(void);
+/* The last CUDA error string seen by the library (thread-local). */
+const char* lpq_last_cuda_error(void);
+
+/* ---- device entry points (stream-ordered, no allocation) ---------------- */
+
+/* quantize_fused_at (proj/src/quant_ops.cpp:154-164) on device memory.
+ *   x, y        : device fp32, row-major, numel = prod(shape); y may equal x
+ *   index_base  : flat index of x[0] in the full tensor (RNG counter offset
+ *                 for shards; 0 for a whole tensor)
+ *   mode        : lpq_rounding; seed/call: RngStream seed and call id
+ *   ws          : device workspace of >= lpq_workspace_size() bytes
+ *   d_status    : device uint32 the kernels OR error bits into (the caller
+ *                 zeroes it; read it with lpq_status_fetch)
+ *   stream      : cudaStream_t (NULL = legacy default stream) */
+lpq_status lpq_quantize(const float* x, float* y, const int64_t* shape,
+                        int rank, uint64_t index_base, const lpq_format* f,
+                        int mode, uint64_t seed, uint64_t call, void* ws,
+                        size_t ws_bytes, uint32_t* d_status, void* stream);
+
+/* Synchronise `stream`, read and clear *d_status, map the bits to a status
+ * (LPQ_ERR_BLOCK_RANGE takes precedence over LPQ_ERR_INVALID_INPUT, as the
+ * reference's reduction pass throws before its quantization pass). */
+lpq_status lpq_status_fetch(uint32_t* d_status, void* stream);
+
+/* Per-op-rounded GEMM (no reference implementation; restated in
+ * oracle/lpq_oracle.h from quant_ops.cpp + scalar_quant.hpp primitives):
+ *   C[i][j]: acc = +0; for k = 0..K-1 (sequential):
+ *              acc = Q_add(fl32(acc + Q_mul(fl32(A[i][k] * B[k][j]))))
+ * A is MxK, B is KxN, C is MxN, row-major device fp32.  fmul/fadd must be
+ * float formats.  Stochastic variates: (seed, call + 2k) for Q_mul and
+ * (seed, call + 2k + 1) for Q_add, index (row_base + i) * N + j.
+ * ws: lpq_quant_gemm_workspace_size() bytes (pre-scan results). */
+size_t lpq_quant_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
+lpq_status lpq_quant_gemm(const float* A, const float* B, float* C, int64_t M,
+                          int64_t N, int64_t K, int64_t row_base,
+                          const lpq_format* fmul, const lpq_format* fadd,
+                          int mode, uint64_t seed, uint64_t call, void* ws,
+                          size_t ws_bytes, uint32_t* d_status, void* stream);
+
+/* quantized_matmul (proj/src/quant_ops.cpp:191-193 over tensor.cpp:355-376):
+ * C = Q(float(sum_k double(A[i][k]) * double(B[k][j]))), double accumulator,
+ * ascending k, quantization fused into the epilogue.  Q's variate index is
+ * (row_base + i) * N + j with (seed, call).  Block formats quantize the
+ * finished product with lpq_quantize (ws: lpq_workspace_size({M, N})). */
+lpq_status lpq_matmul_q(const float* A, const float* B, float* C, int64_t M,
+                        int64_t N, int64_t K, int64_t row_base,
+                        const lpq_format* f, int mode, uint64_t seed,
+                        uint64_t call, void* ws, size_t ws_bytes,
+                        uint32_t* d_status, void* stream);
+
+/* random_uniform (proj/src/tensor.cpp:430-440) over flat indices
+ * [index_base, index_base + n): y[i] = float(lo + (hi - lo) * u). */
+lpq_status lpq_uniform(float* y, int64_t n, uint64_t index_base, uint64_t seed,
+                       uint64_t call, float lo, float hi, void* stream);
+
+/* variate_tensor (proj/src/tensor.cpp:281-290): y[i] = uniform_variate(seed,
+ * call, index_base + i). */
+lpq_status lpq_variates(float* y, int64_t n, uint64_t index_base,
+                        uint64_t seed, uint64_t call, void* stream);
+
+/* ---- host entry points (synchronous; host buffers) ---------------------- */
+
+/* quantize_fused_at over host memory on CUDA device `device` (-1 = current):
+ * H2D, kernels and D2H are pipelined in chunks. */
+lpq_status lpq_quantize_host(const float* x, float* y, const int64_t* shape,
+                             int rank, uint64_t index_base,
+                             const lpq_format* f, int mode, uint64_t seed,
+                             uint64_t call, int device);
+
+lpq_status lpq_quant_gemm_host(const float* A, const float* B, float* C,
+                               int64_t M, int64_t N, int64_t K,
+                               int64_t row_base, const lpq_format* fmul,
+                               const lpq_format* fadd, int mode, uint64_t seed,
+                               uint64_t call, int device);
+
+lpq_status lpq_matmul_q_host(const float* A, const float* B, float* C,
+                             int64_t M, int64_t N, int64_t K,
+                             const lpq_format* f, int mode, uint64_t seed,
+                             uint64_t call, int device);
+
+/* Release the per-device contexts the host entry points created. */
+void lpq_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LPQ_H */

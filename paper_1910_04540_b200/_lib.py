@@ -1,0 +1,138 @@
+"""ctypes binding of liblpq.so (include/lpq.h).
+
+This is the Python-side reference binding of the C ABI (INTEGRATION.md shows
+the same stub for a maintainer).  There is no fallback: if the library is
+missing the import fails loudly, and every status code maps to the exception
+type the reference raises (proj/include/lpsim/errors.hpp:9-55).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "liblpq.so")
+
+OK = 0
+ERR_FORMAT, ERR_SHAPE, ERR_INVALID_INPUT, ERR_UNSUPPORTED = 1, 2, 3, 4
+ERR_BLOCK_RANGE, ERR_ARGUMENT, ERR_WORKSPACE, ERR_CUDA, ERR_NO_DEVICE = 5, 6, 7, 8, 9
+
+
+class LpqFormat(C.Structure):
+    """lpq_format (include/lpq.h) -- one NumberFormat as a flat struct."""
+    _fields_ = [(n, C.c_int32) for n in (
+        "kind", "exp_bits", "man_bits", "wl", "fl", "symmetric", "saturate",
+        "block_dim")]
+
+
+# ---- exception taxonomy of the reference (errors.hpp) ----------------------
+class LpsimError(RuntimeError):
+    pass
+
+
+class InvalidInputError(LpsimError):
+    """invalid_input_error: non-finite input or block maximum out of range."""
+
+
+class ShapeError(LpsimError):
+    """shape_error."""
+
+
+class FormatError(LpsimError):
+    """format_error."""
+
+
+class UnsupportedFormatError(LpsimError):
+    """unsupported_format_error."""
+
+
+class DeviceError(LpsimError):
+    """CUDA runtime failure inside liblpq (no reference counterpart)."""
+
+
+_EXC = {
+    ERR_FORMAT: FormatError, ERR_SHAPE: ShapeError,
+    ERR_INVALID_INPUT: InvalidInputError, ERR_BLOCK_RANGE: InvalidInputError,
+    ERR_UNSUPPORTED: UnsupportedFormatError, ERR_ARGUMENT: ValueError,
+    ERR_WORKSPACE: ValueError, ERR_CUDA: DeviceError, ERR_NO_DEVICE: DeviceError,
+}
+
+_F = C.POINTER(LpqFormat)
+_I64P = C.POINTER(C.c_int64)
+_VP = C.c_void_p
+
+_PROTOS = {
+    "lpq_abi_version": (C.c_int, []),
+    "lpq_status_string": (C.c_char_p, [C.c_int]),
+    "lpq_validate_format": (C.c_int, [_F]),
+    "lpq_workspace_size": (C.c_size_t, [_F, _I64P, C.c_int]),
+    "lpq_launch_count": (C.c_uint64, []),
+    "lpq_pass_count": (C.c_uint64, []),
+    "lpq_reset_pass_count": (None, []),
+    "lpq_last_cuda_error": (C.c_char_p, []),
+    "lpq_quantize": (C.c_int, [_VP, _VP, _I64P, C.c_int, C.c_uint64, _F,
+                               C.c_int, C.c_uint64, C.c_uint64, _VP,
+                               C.c_size_t, _VP, _VP]),
+    "lpq_status_fetch": (C.c_int, [_VP, _VP]),
+    "lpq_quant_gemm_workspace_size": (C.c_size_t, [C.c_int64, C.c_int64,
+                                                   C.c_int64]),
+    "lpq_quant_gemm": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,
+                                 C.c_int64, C.c_int64, _F, _F, C.c_int,
+                                 C.c_uint64, C.c_uint64, _VP, C.c_size_t, _VP,
+                                 _VP]),
+    "lpq_matmul_q": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,
+                               C.c_int64, C.c_int64, _F, C.c_int, C.c_uint64,
+                               C.c_uint64, _VP, C.c_size_t, _VP, _VP]),
+    "lpq_uniform": (C.c_int, [_VP, C.c_int64, C.c_uint64, C.c_uint64,
+                              C.c_uint64, C.c_float, C.c_float, _VP]),
+    "lpq_variates": (C.c_int, [_VP, C.c_int64, C.c_uint64, C.c_uint64,
+                               C.c_uint64, _VP]),
+    "lpq_quantize_host": (C.c_int, [_VP, _VP, _I64P, C.c_int, C.c_uint64, _F,
+                                    C.c_int, C.c_uint64, C.c_uint64,
+                                    C.c_int]),
+    "lpq_quant_gemm_host": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,
+                                      C.c_int64, C.c_int64, _F, _F, C.c_int,
+                                      C.c_uint64, C.c_uint64, C.c_int]),
+    "lpq_matmul_q_host": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,
+                                    C.c_int64, _F, C.c_int, C.c_uint64,
+                                    C.c_uint64, C.c_int]),
+    "lpq_shutdown": (None, []),
+}
+
+# the symbols include/lpq.h declares (tests check every one is exported)
+EXPORTED = tuple(_PROTOS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"liblpq.so not built ({LIB_PATH}); run "
+            "`python -m paper_1910_04540_b200._build` (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _PROTOS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def status_string(st: int) -> str:
+    return lib.lpq_status_string(st).decode()
+
+
+def check(st: int, what: str = "lpq") -> None:
+    """Raise the reference's exception type for a non-OK status."""
+    if st == OK:
+        return
+    msg = f"{what}: {status_string(st)}"
+    if st in (ERR_CUDA, ERR_NO_DEVICE):
+        msg += f" ({lib.lpq_last_cuda_error().decode()})"
+    raise _EXC.get(st, LpsimError)(msg)
+
+
+def shape_array(shape):
+    arr = (C.c_int64 * max(1, len(shape)))(*[int(s) for s in shape])
+    return arr

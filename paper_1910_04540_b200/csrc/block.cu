@@ -1,0 +1,429 @@
+// block.cu -- block-floating-point quantizers (shared exponent per block).
+//
+// Replaces fused_block (proj/src/quant_ops.cpp:68-115) and the block-maximum
+// reduction it calls, reduce_max_abs (proj/src/tensor.cpp:320-353).  The
+// tensor is viewed as [outer, extent, stride]; block b is the slice at index
+// b along `extent` (formats.hpp:69-78).  Three plans:
+//
+//  * kRowsInRegisters (outer == 1, contiguous block <= 32768 floats, aligned):
+//    ONE HBM pass.  One CTA per block ("row"): the row is loaded into
+//    registers with 128-bit loads, max-reduced with warp REDUX + shared
+//    memory, the shared exponent derived in registers, the row quantized and
+//    stored.  8 algorithmic bytes per element.  (BASELINE config C3.)
+//  * kTwoPassSegments (stride >= 1024): pass 1 reduces 4096-element pieces
+//    of each contiguous segment to one atomicMax on the block's maximum;
+//    pass 2 re-reads and quantizes with one shared scale per piece.
+//  * kTwoPassColumns (stride < 1024): the tensor as a [outer, extent*stride]
+//    matrix; each thread owns 4 columns for a chunk of rows and keeps their
+//    maxima in registers (shared-memory atomics once per column, global
+//    atomics once per block touched); pass 2 derives each column's scale once
+//    and streams the rows.
+//  Two-pass plans move 12 algorithmic bytes per element.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace lpq {
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t max4(const float4& v) {
+  return max(max(absbits_for_max(v.x), absbits_for_max(v.y)),
+             max(absbits_for_max(v.z), absbits_for_max(v.w)));
+}
+__device__ __forceinline__ uint32_t nf4(const float4& v) {
+  return (nonfinite(v.x) | nonfinite(v.y) | nonfinite(v.z) | nonfinite(v.w))
+             ? 1u : 0u;
+}
+
+template <int M>
+__device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
+                                    float kmax, uint64_t key, uint64_t idx) {
+  uint32_t v = 0;
+  if (M == kStochastic) v = variate24(key, idx);
+  const float q = quant_block<M>(x, s, kmin, kmax, v);
+  return nonfinite(x) ? 0.0f : q;
+}
+
+template <int M>
+__device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
+                                      float kmin, float kmax, uint64_t key,
+                                      uint64_t idx) {
+  float4 o;
+  o.x = qb<M>(x.x, s, kmin, kmax, key, idx);
+  o.y = qb<M>(x.y, s, kmin, kmax, key, idx + 1);
+  o.z = qb<M>(x.z, s, kmin, kmax, key, idx + 2);
+  o.w = qb<M>(x.w, s, kmin, kmax, key, idx + 3);
+  return o;
+}
+
+__device__ __forceinline__ void flag(uint32_t* status, uint32_t bits) {
+  if (bits) atomicOr(status, bits);
+}
+
+// ---------------------------------------------------------------------------
+// Plan 1: one row per CTA, held in registers (single HBM pass).
+// T threads, VPT float4 per thread; row length L (multiple of 4, <= 4*T*VPT).
+template <int M, int T, int VPT>
+__global__ void __launch_bounds__(T)
+    k_block_rows(const float* __restrict__ x, float* __restrict__ y, int64_t L,
+                 int64_t nrows, uint64_t base, uint64_t key, int wl,
+                 uint32_t* __restrict__ status) {
+  __shared__ uint32_t red[T / 32];
+  __shared__ uint32_t row_max;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float kmin = -(float)(1 << (wl - 1));
+  const float kmax = (float)((1 << (wl - 1)) - 1);
+  const int64_t L4 = L >> 2;
+  uint32_t bad = 0;
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
+    float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
+    float4 v[VPT];
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * T;
+      if (j < L4) {
+        v[k] = __ldcs(xr + j);
+        m = max(m, max4(v[k]));
+        bad |= nf4(v[k]);
+      }
+    }
+    m = __reduce_max_sync(kFull, m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t t = lane < T / 32 ? red[lane] : 0u;
+      t = __reduce_max_sync(kFull, t);
+      if (lane == 0) row_max = t;
+    }
+    __syncthreads();
+    const BlockScale sc = make_block_scale(row_max, wl);
+    if (sc.bad) bad |= 2u;
+    const uint64_t row_base = base + (uint64_t)(r * L);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int64_t j = threadIdx.x + (int64_t)k * T;
+      if (j < L4)
+        __stcs(yr + j, qb4<M>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+    }
+    __syncthreads();  // red/row_max are reused by the next row
+  }
+  bad = __reduce_or_sync(kFull, bad);
+  if (lane == 0) flag(status, bad);
+}
+
+template <int M, int T, int VPT>
+void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
+                   uint64_t base, uint64_t key, int wl, uint32_t* st,
+                   cudaStream_t s) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                k_block_rows<M, T, VPT>, T, 0);
+  const int64_t cap = (int64_t)device_info().sm_count * std::max(per_sm, 1);
+  const int grid = (int)std::max<int64_t>(1, std::min(cap, nrows));
+  k_block_rows<M, T, VPT><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, st);
+  note_launch();
+}
+
+template <int M>
+void launch_rows(const float* x, float* y, int64_t L, int64_t nrows,
+                 uint64_t base, uint64_t key, int wl, uint32_t* st,
+                 cudaStream_t s) {
+  const int64_t L4 = L >> 2;
+  if (L4 <= 128) launch_rows_t<M, 128, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 256) launch_rows_t<M, 256, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 512) launch_rows_t<M, 256, 2>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 1024) launch_rows_t<M, 256, 4>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 2048) launch_rows_t<M, 512, 4>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 4096) launch_rows_t<M, 1024, 4>(x, y, L, nrows, base, key, wl, st, s);
+  else launch_rows_t<M, 1024, 8>(x, y, L, nrows, base, key, wl, st, s);
+}
+
+// ---------------------------------------------------------------------------
+// Plan 2: long contiguous segments (stride >= 1024).  Work item = a piece of
+// kPiece elements inside one segment; every element of a piece shares b.
+constexpr int kSegT = 256;
+constexpr int kPiece = kSegT * 4 * 4;  // 4096 elements, 4 float4 per thread
+
+template <bool VEC>
+__global__ void __launch_bounds__(kSegT)
+    k_seg_reduce(const float* __restrict__ x, int64_t nseg, int64_t stride,
+                 int64_t extent, int64_t pieces, uint32_t* __restrict__ maxima) {
+  __shared__ uint32_t red[kSegT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t items = nseg * pieces;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t seg = it / pieces, pc = it - seg * pieces;
+    const int64_t off = pc * kPiece;
+    const int64_t len = min((int64_t)kPiece, stride - off);
+    const float* xs = x + seg * stride + off;
+    uint32_t m = 0;
+    if (VEC) {
+      const float4* x4 = reinterpret_cast<const float4*>(xs);
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = threadIdx.x + k * kSegT;
+        if (4 * j < len) v[k] = __ldcs(x4 + j);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (4 * (threadIdx.x + k * kSegT) < len) m = max(m, max4(v[k]));
+    } else {
+      for (int j = threadIdx.x; j < len; j += kSegT)
+        m = max(m, absbits_for_max(xs[j]));
+    }
+    m = __reduce_max_sync(kFull, m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t t = lane < kSegT / 32 ? red[lane] : 0u;
+      t = __reduce_max_sync(kFull, t);
+      if (lane == 0 && t) atomicMax(maxima + (seg % extent), t);
+    }
+    __syncthreads();
+  }
+}
+
+template <int M, bool VEC>
+__global__ void __launch_bounds__(kSegT)
+    k_seg_apply(const float* __restrict__ x, float* __restrict__ y,
+                int64_t nseg, int64_t stride, int64_t extent, int64_t pieces,
+                const uint32_t* __restrict__ maxima, uint64_t base,
+                uint64_t key, int wl, uint32_t* __restrict__ status) {
+  const float kmin = -(float)(1 << (wl - 1));
+  const float kmax = (float)((1 << (wl - 1)) - 1);
+  const int64_t items = nseg * pieces;
+  uint32_t bad = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t seg = it / pieces, pc = it - seg * pieces;
+    const int64_t off = pc * kPiece;
+    const int64_t len = min((int64_t)kPiece, stride - off);
+    const int64_t e0 = seg * stride + off;
+    const BlockScale sc = make_block_scale(__ldg(maxima + (seg % extent)), wl);
+    if (sc.bad) bad |= 2u;
+    if (VEC) {
+      const float4* x4 = reinterpret_cast<const float4*>(x + e0);
+      float4* y4 = reinterpret_cast<float4*>(y + e0);
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = threadIdx.x + k * kSegT;
+        if (4 * j < len) v[k] = __ldcs(x4 + j);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = threadIdx.x + k * kSegT;
+        if (4 * j < len) {
+          bad |= nf4(v[k]);
+          __stcs(y4 + j, qb4<M>(v[k], sc, kmin, kmax, key,
+                                base + (uint64_t)(e0 + 4 * j)));
+        }
+      }
+    } else {
+      for (int j = threadIdx.x; j < len; j += kSegT) {
+        const float xv = x[e0 + j];
+        bad |= nonfinite(xv) ? 1u : 0u;
+        y[e0 + j] = qb<M>(xv, sc, kmin, kmax, key, base + (uint64_t)(e0 + j));
+      }
+    }
+  }
+  bad = __reduce_or_sync(kFull, bad);
+  if ((threadIdx.x & 31) == 0) flag(status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Plan 3: short segments (stride < 1024): [outer, W = extent*stride] matrix,
+// 4 columns per thread (a float4 when W % 4 == 0 and aligned), row chunks.
+constexpr int kColT = 256;
+constexpr int kColTile = kColT * 4;  // columns per CTA
+
+template <bool VEC>
+__device__ __forceinline__ float4 load4(const float* __restrict__ row, int64_t c,
+                                        int64_t W) {
+  if (VEC) return __ldcs(reinterpret_cast<const float4*>(row + c));
+  float4 v;
+  v.x = c < W ? row[c] : 0.0f;
+  v.y = c + 1 < W ? row[c + 1] : 0.0f;
+  v.z = c + 2 < W ? row[c + 2] : 0.0f;
+  v.w = c + 3 < W ? row[c + 3] : 0.0f;
+  return v;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kColT)
+    k_col_reduce(const float* __restrict__ x, int64_t outer, int64_t W,
+                 int64_t stride, int64_t rows_per_chunk,
+                 uint32_t* __restrict__ maxima) {
+  __shared__ uint32_t smax[kColTile];  // indexed by b - b0 (<= kColTile)
+  const int64_t c0 = (int64_t)blockIdx.x * kColTile;
+  const int64_t c = c0 + 4 * threadIdx.x;
+  const int64_t b0 = c0 / stride;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t r1 = min(outer, r0 + rows_per_chunk);
+  for (int i = threadIdx.x; i < kColTile; i += kColT) smax[i] = 0u;
+  __syncthreads();
+  if (c < W) {
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+      const float4 v = load4<VEC>(x + r * W, c, W);
+      m0 = max(m0, absbits_for_max(v.x));
+      m1 = max(m1, absbits_for_max(v.y));
+      m2 = max(m2, absbits_for_max(v.z));
+      m3 = max(m3, absbits_for_max(v.w));
+    }
+    atomicMax(&smax[c / stride - b0], m0);
+    if (c + 1 < W) atomicMax(&smax[(c + 1) / stride - b0], m1);
+    if (c + 2 < W) atomicMax(&smax[(c + 2) / stride - b0], m2);
+    if (c + 3 < W) atomicMax(&smax[(c + 3) / stride - b0], m3);
+  }
+  __syncthreads();
+  const int64_t cend = min(W, c0 + kColTile);
+  const int64_t nb = (cend - 1) / stride - b0 + 1;
+  for (int64_t i = threadIdx.x; i < nb; i += kColT)
+    if (smax[i]) atomicMax(maxima + b0 + i, smax[i]);
+}
+
+template <int M, bool VEC>
+__global__ void __launch_bounds__(kColT)
+    k_col_apply(const float* __restrict__ x, float* __restrict__ y,
+                int64_t outer, int64_t W, int64_t stride,
+                int64_t rows_per_chunk, const uint32_t* __restrict__ maxima,
+                uint64_t base, uint64_t key, int wl,
+                uint32_t* __restrict__ status) {
+  const float kmin = -(float)(1 << (wl - 1));
+  const float kmax = (float)((1 << (wl - 1)) - 1);
+  const int64_t c = (int64_t)blockIdx.x * kColTile + 4 * threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t r1 = min(outer, r0 + rows_per_chunk);
+  uint32_t bad = 0;
+  if (c < W) {
+    BlockScale s[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t cq = min(c + q, W - 1);
+      s[q] = make_block_scale(__ldg(maxima + cq / stride), wl);
+      if (s[q].bad) bad |= 2u;
+    }
+    for (int64_t r = r0; r < r1; ++r) {
+      const float4 v = load4<VEC>(x + r * W, c, W);
+      const uint64_t idx = base + (uint64_t)(r * W + c);
+      float4 o;
+      o.x = qb<M>(v.x, s[0], kmin, kmax, key, idx);
+      o.y = qb<M>(v.y, s[1], kmin, kmax, key, idx + 1);
+      o.z = qb<M>(v.z, s[2], kmin, kmax, key, idx + 2);
+      o.w = qb<M>(v.w, s[3], kmin, kmax, key, idx + 3);
+      if (VEC) {
+        bad |= nf4(v);
+        __stcs(reinterpret_cast<float4*>(y + r * W + c), o);
+      } else {
+        float* yr = y + r * W;
+        bad |= nonfinite(v.x) ? 1u : 0u;
+        yr[c] = o.x;
+        if (c + 1 < W) { bad |= nonfinite(v.y) ? 1u : 0u; yr[c + 1] = o.y; }
+        if (c + 2 < W) { bad |= nonfinite(v.z) ? 1u : 0u; yr[c + 2] = o.z; }
+        if (c + 3 < W) { bad |= nonfinite(v.w) ? 1u : 0u; yr[c + 3] = o.w; }
+      }
+    }
+  }
+  bad = __reduce_or_sync(kFull, bad);
+  if ((threadIdx.x & 31) == 0) flag(status, bad);
+}
+
+bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+int64_t col_rows_per_chunk(int64_t outer, int64_t W) {
+  // aim at >= ~16K elements per CTA so register maxima amortise the atomics,
+  // while keeping >= ~4 waves of CTAs on 148 SMs when the tensor is large.
+  const int64_t tiles = (W + kColTile - 1) / kColTile;
+  int64_t r = std::max<int64_t>(16, (int64_t)(16384 / kColTile));
+  const int64_t target_ctas = (int64_t)device_info().sm_count * 8;
+  while (r > 16 && tiles * ((outer + r - 1) / r) < target_ctas) r /= 2;
+  return std::max<int64_t>(1, std::min(r, outer));
+}
+
+template <int M>
+cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
+                           BlockPlan plan, uint64_t base, uint64_t key, int wl,
+                           void* ws, uint32_t* status, cudaStream_t s) {
+  const int64_t n = g.outer * g.extent * g.stride;
+  if (n <= 0) return cudaSuccess;
+  if (plan == BlockPlan::kRowsInRegisters) {
+    launch_rows<M>(x, y, g.stride, g.extent, base, key, wl, status, s);
+    return cudaGetLastError();
+  }
+  uint32_t* maxima = static_cast<uint32_t*>(ws);
+  cudaError_t e = cudaMemsetAsync(maxima, 0, sizeof(uint32_t) * g.extent, s);
+  if (e != cudaSuccess) return e;
+  const int sms = device_info().sm_count;
+  if (plan == BlockPlan::kTwoPassSegments) {
+    const int64_t nseg = g.outer * g.extent;
+    const int64_t pieces = (g.stride + kPiece - 1) / kPiece;
+    const bool vec = (g.stride % 4 == 0) && aligned16(x) && aligned16(y);
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)sms * 8, nseg * pieces));
+    if (vec) {
+      k_seg_reduce<true><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+      k_seg_apply<M, true><<<grid, kSegT, 0, s>>>(x, y, nseg, g.stride, g.extent, pieces,
+                                                  maxima, base, key, wl, status);
+    } else {
+      k_seg_reduce<false><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+      k_seg_apply<M, false><<<grid, kSegT, 0, s>>>(x, y, nseg, g.stride, g.extent, pieces,
+                                                   maxima, base, key, wl, status);
+    }
+    note_launch(2);
+    return cudaGetLastError();
+  }
+  const int64_t W = g.extent * g.stride;
+  const bool vec = (W % 4 == 0) && aligned16(x) && aligned16(y);
+  const int64_t rpc = col_rows_per_chunk(g.outer, W);
+  dim3 grid((unsigned)((W + kColTile - 1) / kColTile),
+            (unsigned)((g.outer + rpc - 1) / rpc));
+  if (vec) {
+    k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+    k_col_apply<M, true><<<grid, kColT, 0, s>>>(x, y, g.outer, W, g.stride, rpc, maxima,
+                                                base, key, wl, status);
+  } else {
+    k_col_reduce<false><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+    k_col_apply<M, false><<<grid, kColT, 0, s>>>(x, y, g.outer, W, g.stride, rpc, maxima,
+                                                 base, key, wl, status);
+  }
+  note_launch(2);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
+  if (g.outer == 1 && g.stride % 4 == 0 && g.stride <= 32768 &&
+      g.stride >= 64 && aligned16(x) && aligned16(y))
+    return BlockPlan::kRowsInRegisters;
+  if (g.stride >= 1024) return BlockPlan::kTwoPassSegments;
+  return BlockPlan::kTwoPassColumns;
+}
+
+size_t block_workspace(const BlockGeom& g, BlockPlan p) {
+  if (p == BlockPlan::kRowsInRegisters) return 0;
+  return (size_t)(((g.extent * 4) + 255) / 256 * 256);
+}
+
+cudaError_t launch_block(const float* x, float* y, const BlockGeom& g,
+                         BlockPlan plan, uint64_t base, uint64_t key, int wl,
+                         int mode, void* ws, uint32_t* status, cudaStream_t s) {
+  switch (mode) {
+    case kStochastic: return launch_block_m<kStochastic>(x, y, g, plan, base, key, wl, ws, status, s);
+    case kNearestAway: return launch_block_m<kNearestAway>(x, y, g, plan, base, key, wl, ws, status, s);
+    case kNearestZero: return launch_block_m<kNearestZero>(x, y, g, plan, base, key, wl, ws, status, s);
+    default: return launch_block_m<kNearestEven>(x, y, g, plan, base, key, wl, ws, status, s);
+  }
+}
+
+}  // namespace lpq

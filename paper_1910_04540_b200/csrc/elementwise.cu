@@ -1,0 +1,204 @@
+// elementwise.cu -- single-pass float / fixed quantizers and the device-side
+// generators (random_uniform, variate_tensor).
+//
+// Replaces the per-element CPU loops fused_fixed / fused_float
+// (proj/src/quant_ops.cpp:33-66) driven by quant_pass/parallel_for
+// (quant_ops.cpp:13-31, tensor.cpp:118-136).  HBM-bound: 8 algorithmic bytes
+// per element.  Each thread moves U float4 per trip with the loads issued
+// before any arithmetic (U*16 B in flight per thread), streaming cache hints
+// (ld.global.cs / st.global.cs), and a grid sized to the resident-CTA count
+// of the 148 SMs, looping grid-stride.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace lpq {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+struct FixedSatOp {
+  FixedParams p;
+  template <int M>
+  __device__ __forceinline__ float apply(float x, uint32_t v) const {
+    return quant_fixed<M, true>(x, p, v);
+  }
+};
+struct FixedWrapOp {
+  FixedParams p;
+  template <int M>
+  __device__ __forceinline__ float apply(float x, uint32_t v) const {
+    return quant_fixed<M, false>(x, p, v);
+  }
+};
+struct FloatOp {
+  FloatParams p;
+  template <int M>
+  __device__ __forceinline__ float apply(float x, uint32_t v) const {
+    return quant_float<M>(x, p, v);
+  }
+};
+
+template <int M, class Op>
+__device__ __forceinline__ float qelem(const Op& op, float x, uint64_t key,
+                                       uint64_t idx, uint32_t& bad) {
+  uint32_t v = 0;
+  if (M == kStochastic) v = variate24(key, idx);
+  const bool nf = nonfinite(x);
+  bad |= nf ? 1u : 0u;
+  const float q = op.template apply<M>(x, v);
+  return nf ? 0.0f : q;  // quant_ops.cpp:21-25: non-finite writes 0
+}
+
+template <int M, class Op>
+__global__ void __launch_bounds__(kThreads)
+    k_elementwise(const float* __restrict__ x, float* __restrict__ y,
+                  int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
+                  uint32_t* __restrict__ status) {
+  const int64_t n4 = (n - head) >> 2;
+  const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
+  float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
+  uint32_t bad = 0;
+  const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
+       i0 < n4; i0 += step) {
+    float4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t j = i0 + (int64_t)u * kThreads;
+      if (j < n4) v[u] = __ldcs(x4 + j);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t j = i0 + (int64_t)u * kThreads;
+      if (j < n4) {
+        const uint64_t idx = base + (uint64_t)(head + 4 * j);
+        float4 o;
+        o.x = qelem<M>(op, v[u].x, key, idx, bad);
+        o.y = qelem<M>(op, v[u].y, key, idx + 1, bad);
+        o.z = qelem<M>(op, v[u].z, key, idx + 2, bad);
+        o.w = qelem<M>(op, v[u].w, key, idx + 3, bad);
+        __stcs(y4 + j, o);
+      }
+    }
+  }
+  // scalar head (before 16-byte alignment) and tail (after the last float4)
+  const int64_t tail0 = head + 4 * n4;
+  const int64_t extra = head + (n - tail0);
+  for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < extra;
+       t += (int64_t)gridDim.x * kThreads) {
+    const int64_t e = t < head ? t : tail0 + (t - head);
+    y[e] = qelem<M>(op, x[e], key, base + (uint64_t)e, bad);
+  }
+  if (__any_sync(0xFFFFFFFFu, bad != 0) && (threadIdx.x & 31) == 0)
+    atomicOr(status, kStatusNonFinite);
+}
+
+int64_t vector_head(const float* x, const float* y, int64_t n) {
+  const uintptr_t ax = reinterpret_cast<uintptr_t>(x);
+  const uintptr_t ay = reinterpret_cast<uintptr_t>(y);
+  if (((ax ^ ay) & 15u) != 0) return n;  // different misalignment: scalar
+  const int64_t h = (int64_t)(((16u - (ax & 15u)) & 15u) >> 2);
+  return std::min(h, n);
+}
+
+template <int M, class Op>
+cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
+                      uint64_t key, const Op& op, uint32_t* status,
+                      cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t head = vector_head(x, y, n);
+  const int64_t n4 = (n - head) >> 2;
+  const int64_t work = std::max<int64_t>(n4, n - 4 * n4);
+  const DeviceInfo& di = device_info();
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_elementwise<M, Op>,
+                                                kThreads, 0);
+  const int64_t cap = (int64_t)di.sm_count * std::max(per_sm, 1);
+  const int64_t want = (work + (int64_t)kThreads * kUnroll - 1) /
+                       ((int64_t)kThreads * kUnroll);
+  const int grid = (int)std::max<int64_t>(1, std::min(cap, want));
+  k_elementwise<M, Op><<<grid, kThreads, 0, s>>>(x, y, n, head, base, key, op,
+                                                 status);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <class Op>
+cudaError_t dispatch_mode(const float* x, float* y, int64_t n, uint64_t base,
+                          uint64_t key, const Op& op, int mode,
+                          uint32_t* status, cudaStream_t s) {
+  switch (mode) {
+    case kStochastic: return launch_ew<kStochastic>(x, y, n, base, key, op, status, s);
+    case kNearestAway: return launch_ew<kNearestAway>(x, y, n, base, key, op, status, s);
+    case kNearestZero: return launch_ew<kNearestZero>(x, y, n, base, key, op, status, s);
+    default: return launch_ew<kNearestEven>(x, y, n, base, key, op, status, s);
+  }
+}
+
+// ---- generators -------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads)
+    k_uniform(float* __restrict__ y, int64_t n, uint64_t base, uint64_t key,
+              double lo, double span) {
+  // tensor.cpp:430-440: float(lo + (hi - lo) * u) in double; (hi-lo)*u is
+  // exact (24 x 24 bits), so contraction into DFMA cannot change the result.
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const double u = (double)variate24(key, base + (uint64_t)i) * 0x1p-24;
+    y[i] = __double2float_rn(__dadd_rn(lo, __dmul_rn(span, u)));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_variates(float* __restrict__ y, int64_t n, uint64_t base, uint64_t key) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads)
+    y[i] = variate_float(variate24(key, base + (uint64_t)i));
+}
+
+int gen_grid(int64_t n) {
+  const int64_t cap = (int64_t)device_info().sm_count * 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (n + kThreads - 1) / kThreads));
+}
+
+}  // namespace
+
+cudaError_t launch_fixed(const float* x, float* y, int64_t n, uint64_t base,
+                         uint64_t key, const FixedParams& p, int mode,
+                         uint32_t* status, cudaStream_t s) {
+  if (p.saturate)
+    return dispatch_mode(x, y, n, base, key, FixedSatOp{p}, mode, status, s);
+  return dispatch_mode(x, y, n, base, key, FixedWrapOp{p}, mode, status, s);
+}
+
+cudaError_t launch_float(const float* x, float* y, int64_t n, uint64_t base,
+                         uint64_t key, const FloatParams& p, int mode,
+                         uint32_t* status, cudaStream_t s) {
+  return dispatch_mode(x, y, n, base, key, FloatOp{p}, mode, status, s);
+}
+
+cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,
+                           float lo, float hi, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const double l = lo, h = hi;
+  k_uniform<<<gen_grid(n), kThreads, 0, s>>>(y, n, base, key, l, h - l);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_variates(float* y, int64_t n, uint64_t base, uint64_t key,
+                            cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_variates<<<gen_grid(n), kThreads, 0, s>>>(y, n, base, key);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace lpq

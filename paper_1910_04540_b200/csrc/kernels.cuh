@@ -1,0 +1,86 @@
+// kernels.cuh -- launch interfaces of the sm_100a quantizer kernels.
+// Internal to liblpq.so; the public boundary is include/lpq.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "quant_math.cuh"
+
+namespace lpq {
+
+// Error bits the kernels OR into the caller's device status word.
+enum : uint32_t { kStatusNonFinite = 1u, kStatusBlockRange = 2u };
+
+struct DeviceInfo {
+  int sm_count;
+  int max_smem_optin;
+};
+const DeviceInfo& device_info();  // of the current device (cached)
+
+void note_launch(int n = 1);      // library-wide launch counter
+
+// ---- elementwise float / fixed (one HBM pass) ----------------------------
+// x, y: device fp32 (4-byte aligned); n elements; base: flat index of x[0].
+cudaError_t launch_fixed(const float* x, float* y, int64_t n, uint64_t base,
+                         uint64_t key, const FixedParams& p, int mode,
+                         uint32_t* status, cudaStream_t s);
+cudaError_t launch_float(const float* x, float* y, int64_t n, uint64_t base,
+                         uint64_t key, const FloatParams& p, int mode,
+                         uint32_t* status, cudaStream_t s);
+
+// ---- block floating point -------------------------------------------------
+// The tensor is viewed as [outer, extent, stride]; block b = index along
+// `extent` (whole tensor: outer = extent = 1, stride = n).
+struct BlockGeom {
+  int64_t outer;
+  int64_t extent;
+  int64_t stride;
+};
+
+// Which plan a block quantization uses (and how many HBM passes it makes).
+enum class BlockPlan { kRowsInRegisters, kTwoPassSegments, kTwoPassColumns };
+BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y);
+inline int block_plan_passes(BlockPlan p) {
+  return p == BlockPlan::kRowsInRegisters ? 1 : 2;
+}
+// Workspace bytes for a plan: extent uint32 maxima (two-pass plans only).
+size_t block_workspace(const BlockGeom& g, BlockPlan p);
+
+cudaError_t launch_block(const float* x, float* y, const BlockGeom& g,
+                         BlockPlan plan, uint64_t base, uint64_t key, int wl,
+                         int mode, void* ws, uint32_t* status, cudaStream_t s);
+
+// ---- generators -------------------------------------------------------------
+cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,
+                           float lo, float hi, cudaStream_t s);
+cudaError_t launch_variates(float* y, int64_t n, uint64_t base, uint64_t key,
+                            cudaStream_t s);
+
+// ---- GEMMs ------------------------------------------------------------------
+struct GemmScan {        // pre-scan of A and B (device-written)
+  uint32_t a_min_nz_exp_field;  // min exponent field over nonzero |a| (255 if none)
+  uint32_t a_max_exp_field;
+  uint32_t b_min_nz_exp_field;
+  uint32_t b_max_exp_field;
+  uint32_t a_low_bits;          // OR of (bits & 0xFFFF) over A: 0 iff bf16-exact
+  uint32_t b_low_bits;
+  uint32_t nonfinite;           // any non-finite in A or B
+  uint32_t pad;
+};
+
+cudaError_t launch_quant_gemm(const float* A, const float* B, float* C,
+                              int64_t M, int64_t N, int64_t K,
+                              int64_t row_base, const FloatParams& qm,
+                              const FloatParams& qa, bool bf16_formats,
+                              int mode, uint64_t seed, uint64_t call,
+                              GemmScan* scan, uint32_t* status,
+                              cudaStream_t s);
+
+cudaError_t launch_matmul_q(const float* A, const float* B, float* C,
+                            int64_t M, int64_t N, int64_t K, int64_t row_base,
+                            int kind, const FloatParams& fp,
+                            const FixedParams& xp, int mode, uint64_t key,
+                            uint32_t* status, cudaStream_t s);
+
+}  // namespace lpq

@@ -1,0 +1,355 @@
+// runtime.cu -- host-memory entry points of liblpq.so.
+//
+// The reference API takes and returns host tensors (lpsim::Tensor, a
+// std::vector<float>; proj/include/lpsim/tensor.hpp:19-46).  These entry
+// points give that API a B200 path: a per-device context owns three CUDA
+// streams, device chunk buffers and pinned bounce buffers; a call streams the
+// tensor through them so that chunk c's host->device copy, chunk c-1's kernel
+// and chunk c-2's device->host copy run concurrently (two copy engines + the
+// SMs).  Pinned caller memory is copied directly; pageable memory (a plain
+// std::vector, as the drop-in shim passes) is bounced through the pinned
+// buffers with a multi-threaded memcpy.  Block formats whose blocks are not
+// contiguous rows need the whole tensor resident for the reduction pass and
+// take the resident path (copy in, two device passes, copy out).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/lpq.h"
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace lpq {
+
+namespace {
+
+constexpr int kStreams = 3;
+constexpr int64_t kChunkElems = int64_t(1) << 24;  // 64 MiB of fp32
+
+struct HostCtx {
+  int dev = 0;
+  cudaStream_t st[kStreams] = {};
+  cudaEvent_t done[kStreams] = {};
+  float* dbuf[kStreams] = {};
+  float* pin_in[kStreams] = {};
+  float* pin_out[kStreams] = {};
+  int64_t chunk_cap = 0;  // elements per chunk buffer
+  uint32_t* d_status = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  float* dfull = nullptr;
+  int64_t dfull_cap = 0;
+  std::mutex mu;
+
+  ~HostCtx() { release(); }
+
+  void release() {
+    DeviceGuard g(dev);
+    for (int k = 0; k < kStreams; ++k) {
+      if (dbuf[k]) cudaFree(dbuf[k]);
+      if (pin_in[k]) cudaFreeHost(pin_in[k]);
+      if (pin_out[k]) cudaFreeHost(pin_out[k]);
+      if (done[k]) cudaEventDestroy(done[k]);
+      if (st[k]) cudaStreamDestroy(st[k]);
+      dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
+      done[k] = nullptr;
+      st[k] = nullptr;
+    }
+    if (d_status) cudaFree(d_status);
+    if (ws) cudaFree(ws);
+    if (dfull) cudaFree(dfull);
+    d_status = nullptr;
+    ws = nullptr;
+    dfull = nullptr;
+    chunk_cap = dfull_cap = 0;
+    ws_bytes = 0;
+  }
+
+  cudaError_t init() {
+    if (st[0]) return cudaSuccess;
+    for (int k = 0; k < kStreams; ++k) {
+      cudaError_t e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaMalloc(&d_status, sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    return cudaMemset(d_status, 0, sizeof(uint32_t));
+  }
+
+  cudaError_t ensure_chunks(int64_t elems) {
+    if (elems <= chunk_cap) return cudaSuccess;
+    for (int k = 0; k < kStreams; ++k) {
+      if (dbuf[k]) cudaFree(dbuf[k]);
+      if (pin_in[k]) cudaFreeHost(pin_in[k]);
+      if (pin_out[k]) cudaFreeHost(pin_out[k]);
+      dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
+    }
+    chunk_cap = 0;
+    const size_t bytes = sizeof(float) * (size_t)elems;
+    for (int k = 0; k < kStreams; ++k) {
+      cudaError_t e = cudaMalloc(&dbuf[k], bytes);
+      if (e == cudaSuccess) e = cudaMallocHost(&pin_in[k], bytes);
+      if (e == cudaSuccess) e = cudaMallocHost(&pin_out[k], bytes);
+      if (e != cudaSuccess) return e;
+    }
+    chunk_cap = elems;
+    return cudaSuccess;
+  }
+
+  cudaError_t ensure_full(int64_t elems) {
+    if (elems <= dfull_cap) return cudaSuccess;
+    if (dfull) cudaFree(dfull);
+    dfull = nullptr;
+    dfull_cap = 0;
+    cudaError_t e = cudaMalloc(&dfull, sizeof(float) * (size_t)elems);
+    if (e == cudaSuccess) dfull_cap = elems;
+    return e;
+  }
+
+  cudaError_t ensure_ws(size_t bytes) {
+    if (bytes <= ws_bytes) return cudaSuccess;
+    if (ws) cudaFree(ws);
+    ws = nullptr;
+    ws_bytes = 0;
+    cudaError_t e = cudaMalloc(&ws, bytes);
+    if (e == cudaSuccess) ws_bytes = bytes;
+    return e;
+  }
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<HostCtx>> g_ctx;
+
+HostCtx* context_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1);
+  if (!g_ctx[dev]) {
+    g_ctx[dev].reset(new HostCtx());
+    g_ctx[dev]->dev = dev;
+  }
+  return g_ctx[dev].get();
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = size_t(8) << 20;
+  unsigned hw = std::thread::hardware_concurrency();
+  const int T = (int)std::min<size_t>(std::max(1u, std::min(hw, 16u)),
+                                      std::max<size_t>(1, bytes / kMin));
+  if (T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t part = (bytes / T + 63) & ~size_t(63);
+  std::vector<std::thread> pool;
+  pool.reserve(T - 1);
+  for (int t = 1; t < T; ++t) {
+    const size_t b = part * t;
+    if (b >= bytes) break;
+    const size_t len = std::min(part, bytes - b);
+    pool.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + b,
+                  static_cast<const char*>(src) + b, len);
+    });
+  }
+  std::memcpy(dst, src, std::min(part, bytes));
+  for (auto& th : pool) th.join();
+}
+
+int resolve_device(int device, lpq_status* st) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    *st = cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e);
+    return -1;
+  }
+  if (device < 0) cudaGetDevice(&device);
+  if (device >= count) {
+    *st = LPQ_ERR_ARGUMENT;
+    return -1;
+  }
+  *st = LPQ_OK;
+  return device;
+}
+
+#define LPQ_TRY(expr)                          \
+  do {                                         \
+    cudaError_t _e = (expr);                   \
+    if (_e != cudaSuccess) return cuda_fail(_e); \
+  } while (0)
+
+// Streaming path: chunks of `unit`-aligned elements, each quantized as an
+// independent piece with its own flat index base (elementwise formats, or
+// block formats whose blocks are whole contiguous rows of length `unit`).
+lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
+                           int64_t unit, bool rows, uint64_t index_base,
+                           const lpq_format* f, int mode, uint64_t seed,
+                           uint64_t call) {
+  const int64_t chunk = std::max<int64_t>(1, kChunkElems / unit) * unit;
+  LPQ_TRY(c->ensure_chunks(chunk));
+  const bool pin_x = is_pinned(x), pin_y = is_pinned(y);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  lpq_format fr = *f;
+  if (rows) fr.block_dim = 0;
+  lpq_status qst = LPQ_OK;
+  auto finish = [&](int64_t ci) {
+    const int k = (int)(ci % kStreams);
+    cudaEventSynchronize(c->done[k]);
+    if (!pin_y) {
+      const int64_t off = ci * chunk, len = std::min(chunk, n - off);
+      parallel_memcpy(y + off, c->pin_out[k], sizeof(float) * (size_t)len);
+    }
+  };
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int k = (int)(ci % kStreams);
+    if (ci >= kStreams) finish(ci - kStreams);
+    const int64_t off = ci * chunk, len = std::min(chunk, n - off);
+    const size_t bytes = sizeof(float) * (size_t)len;
+    const float* src = x + off;
+    if (!pin_x) {
+      parallel_memcpy(c->pin_in[k], x + off, bytes);
+      src = c->pin_in[k];
+    }
+    float* dst = pin_y ? y + off : c->pin_out[k];
+    LPQ_TRY(cudaMemcpyAsync(c->dbuf[k], src, bytes, cudaMemcpyHostToDevice, c->st[k]));
+    int64_t shp[2];
+    int rank;
+    if (rows) { shp[0] = len / unit; shp[1] = unit; rank = 2; }
+    else { shp[0] = len; rank = 1; }
+    qst = quantize_device(c->dbuf[k], c->dbuf[k], shp, rank,
+                          index_base + (uint64_t)off, &fr, mode, seed, call,
+                          nullptr, 0, c->d_status, c->st[k]);
+    if (qst != LPQ_OK) break;
+    LPQ_TRY(cudaMemcpyAsync(dst, c->dbuf[k], bytes, cudaMemcpyDeviceToHost, c->st[k]));
+    LPQ_TRY(cudaEventRecord(c->done[k], c->st[k]));
+  }
+  for (int64_t ci = std::max<int64_t>(0, nchunks - kStreams); ci < nchunks; ++ci)
+    finish(ci);
+  if (qst != LPQ_OK) {
+    for (int k = 0; k < kStreams; ++k) cudaStreamSynchronize(c->st[k]);
+    return qst;
+  }
+  return lpq_status_fetch(c->d_status, c->st[0]);
+}
+
+// Resident path: the whole tensor on the device (two-pass block formats).
+lpq_status resident_quantize(HostCtx* c, const float* x, float* y,
+                             const int64_t* shape, int rank, int64_t n,
+                             uint64_t index_base, const lpq_format* f,
+                             int mode, uint64_t seed, uint64_t call) {
+  LPQ_TRY(c->ensure_full(n));
+  const size_t wsb = lpq_workspace_size(f, shape, rank);
+  if (wsb) LPQ_TRY(c->ensure_ws(wsb));
+  cudaStream_t s = c->st[0];
+  const size_t bytes = sizeof(float) * (size_t)n;
+  if (is_pinned(x)) {
+    LPQ_TRY(cudaMemcpyAsync(c->dfull, x, bytes, cudaMemcpyHostToDevice, s));
+  } else {
+    LPQ_TRY(c->ensure_chunks(std::min<int64_t>(n, kChunkElems)));
+    for (int64_t off = 0; off < n; off += c->chunk_cap) {
+      const int64_t len = std::min(c->chunk_cap, n - off);
+      const int k = (int)((off / c->chunk_cap) % 2);
+      LPQ_TRY(cudaEventSynchronize(c->done[k]));
+      parallel_memcpy(c->pin_in[k], x + off, sizeof(float) * (size_t)len);
+      LPQ_TRY(cudaMemcpyAsync(c->dfull + off, c->pin_in[k],
+                              sizeof(float) * (size_t)len,
+                              cudaMemcpyHostToDevice, s));
+      LPQ_TRY(cudaEventRecord(c->done[k], s));
+    }
+  }
+  lpq_status qst = quantize_device(c->dfull, c->dfull, shape, rank, index_base,
+                                   f, mode, seed, call, c->ws, c->ws_bytes,
+                                   c->d_status, s);
+  if (qst != LPQ_OK) {
+    cudaStreamSynchronize(s);
+    return qst;
+  }
+  if (is_pinned(y)) {
+    LPQ_TRY(cudaMemcpyAsync(y, c->dfull, bytes, cudaMemcpyDeviceToHost, s));
+  } else {
+    LPQ_TRY(c->ensure_chunks(std::min<int64_t>(n, kChunkElems)));
+    for (int64_t off = 0; off < n; off += c->chunk_cap) {
+      const int64_t len = std::min(c->chunk_cap, n - off);
+      LPQ_TRY(cudaMemcpyAsync(c->pin_out[0], c->dfull + off,
+                              sizeof(float) * (size_t)len,
+                              cudaMemcpyDeviceToHost, s));
+      LPQ_TRY(cudaStreamSynchronize(s));
+      parallel_memcpy(y + off, c->pin_out[0], sizeof(float) * (size_t)len);
+    }
+  }
+  return lpq_status_fetch(c->d_status, s);
+}
+
+}  // namespace
+
+lpq_status host_context_quantize(const float* x, float* y,
+                                 const int64_t* shape, int rank,
+                                 uint64_t index_base, const lpq_format* f,
+                                 int mode, uint64_t seed, uint64_t call,
+                                 int device) {
+  lpq_status st = check_format(f);
+  if (st != LPQ_OK) return st;
+  int64_t n = 0;
+  st = check_shape(shape, rank, &n);
+  if (st != LPQ_OK) return st;
+  if (mode < 0 || mode > 3) return LPQ_ERR_ARGUMENT;
+  BlockGeom g{1, 1, n};
+  if (f->kind == LPQ_BLOCK) {
+    st = block_geometry(f, shape, rank, &g);
+    if (st != LPQ_OK) return st;
+  }
+  if (n == 0) return LPQ_OK;
+  if (!x || !y) return LPQ_ERR_ARGUMENT;
+  const int dev = resolve_device(device, &st);
+  if (dev < 0) return st;
+  DeviceGuard guard(dev);
+  HostCtx* c = context_for(dev);
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaError_t e = c->init();
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (f->kind != LPQ_BLOCK)
+    return stream_quantize(c, x, y, n, 1, false, index_base, f, mode, seed, call);
+  // an aligned device buffer decides the plan exactly as the device call will
+  static const float* kAligned = reinterpret_cast<const float*>(uintptr_t(256));
+  if (block_plan(g, kAligned, kAligned) == BlockPlan::kRowsInRegisters)
+    return stream_quantize(c, x, y, n, g.stride, true, index_base, f, mode,
+                           seed, call);
+  return resident_quantize(c, x, y, shape, rank, n, index_base, f, mode, seed,
+                           call);
+}
+
+void shutdown_contexts() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_ctx.clear();
+}
+
+}  // namespace lpq
+
+extern "C" {
+
+lpq_status lpq_quantize_host(const float* x, float* y, const int64_t* shape,
+                             int rank, uint64_t index_base,
+                             const lpq_format* f, int mode, uint64_t seed,
+                             uint64_t call, int device) {
+  return lpq::host_context_quantize(x, y, shape, rank, index_base, f, mode,
+                                    seed, call, device);
+}
+
+void lpq_shutdown(void) { lpq::shutdown_contexts(); }
+
+}  // extern "C"

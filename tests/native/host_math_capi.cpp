@@ -57,5 +57,8 @@ int hm_quant_block(const float* x, const uint32_t* v, float* y, int64_t n, int w
   return bad;
 }
 uint32_t hm_variate24(uint64_t key, uint64_t index) { return lpq::variate24(key, index); }
+void hm_variates24(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24(key, base + (uint64_t)i);
+}
 uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
 }

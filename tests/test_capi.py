@@ -1,0 +1,80 @@
+"""liblpq.so loads, exports every symbol include/lpq.h declares, and its
+host-only helpers behave without a GPU (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lpq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lpq_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1910_04540_b200 import _lib
+    names = declared_symbols()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(_lib.lib, n), n
+    assert set(names) == set(_lib.EXPORTED)
+
+
+def test_library_is_sm100a_and_loads():
+    from paper_1910_04540_b200 import _lib
+    assert _lib.lib.lpq_abi_version() == 1
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob or b"sm_100" in blob
+
+
+@pytest.mark.parametrize("fmt,ok", [
+    ("float:8:23", True), ("float:0:2", False), ("float:9:2", False),
+    ("float:5:24", False), ("float:1:0", True), ("fixed:2:0", True),
+    ("fixed:1:0", False), ("fixed:25:0", False), ("fixed:8:-120", True),
+    ("fixed:8:-121", False), ("fixed:8:126", True), ("fixed:8:127", False),
+    ("block:8", True), ("block:1", False), ("block:25", False),
+])
+def test_validate_matches_reference_rules(fmt, ok):
+    # formats.hpp:82-112
+    import paper_1910_04540_b200 as q
+    kind, *a = fmt.split(":")
+    a = [int(v) for v in a]
+    f = {"float": q.FloatFormat, "fixed": q.FixedFormat, "block": q.BlockFloatFormat}[kind](*a)
+    if ok:
+        q.validate(f)
+    else:
+        with pytest.raises(q.FormatError):
+            q.validate(f)
+
+
+def test_block_dim_negative_rejected():
+    import paper_1910_04540_b200 as q
+    with pytest.raises(q.FormatError):
+        q.validate(q.BlockFloatFormat(8, -3))
+
+
+def test_workspace_and_status_strings():
+    from paper_1910_04540_b200 import _lib
+    import paper_1910_04540_b200 as q
+    f = q.BlockFloatFormat(8, 1).c()
+    shp = _lib.shape_array((3, 1000, 7))
+    assert _lib.lib.lpq_workspace_size(C.byref(f), shp, 3) >= 1000 * 4
+    assert _lib.lib.lpq_workspace_size(C.byref(q.FixedFormat(8, 4).c()), shp, 3) == 0
+    for s in range(10):
+        assert _lib.status_string(s)
+    assert "non-finite" in _lib.status_string(3)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200._lib import DeviceError
+    with pytest.raises(DeviceError):
+        q.quantize_fused_at(np.ones(16, np.float32), q.QuantSpec(q.FixedFormat(8, 4)), 0)

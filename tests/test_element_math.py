@@ -1,0 +1,112 @@
+"""The kernels' per-element arithmetic (paper_1910_04540_b200/csrc/
+quant_math.cuh), compiled for the host CPU, swept against the oracle.
+
+The same source is inlined into every sm_100a quantizer kernel, so this pins
+the exactness arguments of DESIGN.md §3 on ~10^6 inputs per (format, mode)
+without a GPU: random bit patterns over the whole finite fp32 range, random
+magnitudes 2^-150..2^127, uniform values, and hand-picked edges.  The GPU
+tests then only have to show the kernels apply it to the right elements.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import (ALL_MODES, block_fmt, bits, f32_from_bits, fixed_fmt,
+                        float_fmt, Fmt)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hm():
+    from paper_1910_04540_b200._build import build_host_math
+    path = build_host_math()
+    L = C.CDLL(path)
+    fp = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+    up = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+    L.hm_quant.argtypes = [fp, up, fp, C.c_int64, C.POINTER(Fmt), C.c_int]
+    L.hm_quant_block.argtypes = [fp, up, fp, C.c_int64, C.c_int, C.c_uint32, C.c_int]
+    L.hm_quant_block.restype = C.c_int
+    L.hm_variate24.restype = C.c_uint32
+    L.hm_variate24.argtypes = [C.c_uint64, C.c_uint64]
+    L.hm_stream_key.restype = C.c_uint64
+    L.hm_stream_key.argtypes = [C.c_uint64, C.c_uint64]
+    L.hm_variates24.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    return L
+
+
+def variates(hm, seed, call, n):
+    v = np.empty(n, np.uint32)
+    hm.hm_variates24(hm.hm_stream_key(seed, call), 0, n, v)
+    return v
+
+
+def inputs(n=1 << 18, seed=7):
+    rng = np.random.default_rng(seed)
+    b = f32_from_bits(rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32))
+    mags = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-150, 128, n)).astype(np.float32)
+    u = rng.uniform(-20, 20, n).astype(np.float32)
+    sp = np.array([0.0, -0.0, 0.5, -0.5, 1.5, 2.5, -2.5, 1e-45, -1e-45, 3.99,
+                   0.25, -0.25, 0.75, 114688.0, 122880.0, 3.4028235e38], np.float32)
+    x = np.concatenate([sp, b, mags, u])
+    return x[np.isfinite(x)]
+
+
+FORMATS = [float_fmt(5, 2), float_fmt(8, 7), float_fmt(8, 23), float_fmt(1, 0),
+           float_fmt(2, 1), float_fmt(4, 3), float_fmt(1, 23), float_fmt(8, 0),
+           float_fmt(3, 2), float_fmt(7, 12),
+           fixed_fmt(8, 4), fixed_fmt(3, 1), fixed_fmt(8, 4, True),
+           fixed_fmt(6, 2, False, False), fixed_fmt(5, 2, True, False),
+           fixed_fmt(24, 126), fixed_fmt(2, -126), fixed_fmt(24, -104, False, False),
+           fixed_fmt(24, 100, True, False), fixed_fmt(12, 60, False, False),
+           fixed_fmt(4, -20, False, False)]
+
+
+def test_variate24_matches_reference_rng(hm, oracle):
+    for seed, call in [(1, 0), (0x15EED, 0), (77, 5), (2**64 - 1, 2**63 + 5)]:
+        key = hm.hm_stream_key(seed, call)
+        assert key == oracle.L.lpqo_stream_key(seed, call)
+        for i in list(range(300)) + [2**40 + 3, 2**64 - 1]:
+            assert hm.hm_variate24(key, i) * 2.0**-24 == oracle.variate(seed, call, i)
+
+
+@pytest.mark.parametrize("fmt", FORMATS, ids=repr)
+@pytest.mark.parametrize("mode", ALL_MODES)
+def test_elementwise_math_vs_oracle(hm, oracle, fmt, mode):
+    x = inputs()
+    seed, call = 9 + mode, 3
+    st, want = oracle.quantize(x, fmt, mode, seed=seed, call=call)
+    assert st == 0
+    v = variates(hm, seed, call, x.size) if mode == 0 else np.zeros(x.size, np.uint32)
+    got = np.empty_like(x)
+    hm.hm_quant(x, v, got, x.size, C.byref(fmt), mode)
+    bad = bits(got) != bits(want)
+    assert not bad.any(), (x[bad][:4], got[bad][:4], want[bad][:4])
+
+
+@pytest.mark.parametrize("wl", [2, 3, 4, 8, 12, 24])
+@pytest.mark.parametrize("mode", ALL_MODES)
+def test_block_math_vs_oracle(hm, oracle, wl, mode):
+    rng = np.random.default_rng(wl * 10 + mode)
+    for trial in range(40):
+        e = int(rng.integers(-160, 128))
+        x = (rng.uniform(-1, 1, 301) * 2.0**e).astype(np.float32)
+        if trial % 5 == 0:
+            x[:150] = 0.0
+        if trial == 3:
+            x[:] = 0.0
+        if not np.isfinite(x).all():
+            continue
+        seed, call = 5, trial
+        st, want = oracle.quantize(x, block_fmt(wl), mode, seed=seed, call=call)
+        v = variates(hm, seed, call, x.size)
+        got = np.empty_like(x)
+        badblk = hm.hm_quant_block(x, v, got, x.size, wl,
+                                   int(bits(np.abs(x)).max()), mode)
+        if st == 3:
+            assert badblk
+            continue
+        assert st == 0 and not badblk
+        assert np.array_equal(bits(got), bits(want)), (wl, mode, e)

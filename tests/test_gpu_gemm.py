@@ -1,0 +1,156 @@
+"""GPU parity of the GEMMs.
+
+* quant_gemm (per-op-rounded, lpq_quant_gemm) vs the restated oracle
+  lpqo_quant_gemm: bit-exact, both kernels (hardware-bf16 fast path and the
+  general path), every rounding mode; the rounding ORDER (sequential k, Q after
+  every multiply and add) is the oracle's definition -- "parity unpinned" by
+  any reference test.
+* quantized_matmul (lpq_matmul_q) vs the reference library's own
+  quantized_matmul outputs (golden fixtures) and the oracle's double matmul.
+"""
+import numpy as np
+import pytest
+
+import golden_cases
+from oracle_lib import (ALL_MODES, NEAREST_EVEN, STOCHASTIC, bits, fixed_fmt,
+                        float_fmt)
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1910_04540_b200 as q
+    return q
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def bf16_operands(oracle, shape, seed, lo=-1.0, hi=1.0):
+    n = int(np.prod(shape))
+    x = oracle.random_uniform(n, seed, 0, lo, hi)
+    st, xq = oracle.quantize(x, float_fmt(8, 7), NEAREST_EVEN)
+    return xq.reshape(shape)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 64, 64), (200, 300, 257), (1, 7, 3),
+                                   (129, 131, 1000), (256, 256, 16)])
+def test_quant_gemm_bf16_path_vs_oracle(q, oracle, M, N, K):
+    a = bf16_operands(oracle, (M, K), 1)
+    b = bf16_operands(oracle, (K, N), 2)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    assert st == 0
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_quant_gemm_general_path_non_bf16_inputs(q, oracle):
+    rng = np.random.default_rng(4)
+    a = rng.uniform(-1, 1, (70, 90)).astype(np.float32)   # not bf16-exact
+    b = rng.uniform(-1, 1, (90, 50)).astype(np.float32)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_quant_gemm_underflow_guard(q, oracle):
+    # bf16-exact operands whose products fall below 2^-126: the device-side
+    # pre-scan must route to the general kernel (two-point underflow grid)
+    a = bf16_operands(oracle, (40, 60), 5) * np.float32(2.0**-70)
+    b = bf16_operands(oracle, (60, 30), 6) * np.float32(2.0**-60)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_quant_gemm_overflow_guard(q, oracle):
+    a = bf16_operands(oracle, (20, 64), 7) * np.float32(2.0**70)
+    b = bf16_operands(oracle, (64, 20), 8) * np.float32(2.0**62)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("fm,fa", [((5, 2), (5, 2)), ((8, 7), (8, 7)),
+                                   ((4, 3), (8, 10)), ((8, 23), (8, 23))])
+@pytest.mark.parametrize("mode", ALL_MODES)
+def test_quant_gemm_formats_modes(q, oracle, fm, fa, mode):
+    rng = np.random.default_rng(fm[0] * 10 + fa[1] + mode)
+    a = rng.uniform(-2, 2, (33, 47)).astype(np.float32)
+    b = rng.uniform(-2, 2, (47, 29)).astype(np.float32)
+    st, want = oracle.quant_gemm(a, b, float_fmt(*fm), float_fmt(*fa), mode,
+                                 seed=99, call=4, row_base=5)
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(*fm), q.FloatFormat(*fa),
+                       q.RoundingMode(mode), 99, 4, row_base=5)
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_quant_gemm_host_path(q, oracle):
+    a = bf16_operands(oracle, (50, 70), 11)
+    b = bf16_operands(oracle, (70, 40), 12)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    got = q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_quant_gemm_identity_format_is_fp32_sequential(q):
+    # float(8,23) Q is the identity on normal values: the per-op GEMM then
+    # equals a plain fp32 mul/add chain in ascending k
+    rng = np.random.default_rng(2)
+    a = rng.uniform(-1, 1, (16, 40)).astype(np.float32)
+    b = rng.uniform(-1, 1, (40, 12)).astype(np.float32)
+    want = np.zeros((16, 12), np.float32)
+    for k in range(40):
+        want = (want + (a[:, k:k + 1] * b[k:k + 1, :]).astype(np.float32)).astype(np.float32)
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 23), q.FloatFormat(8, 23))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_c4_quant_gemm_4096_sampled_rows(q, oracle):
+    n = 4096
+    a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
+    b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
+    f87 = q.QuantSpec(q.FloatFormat(8, 7))
+    a = q.quantize_fused_at(a, f87, 0)
+    b = q.quantize_fused_at(b, f87, 0)
+    c = q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7)).cpu().numpy()
+    ah, bh = a.cpu().numpy(), b.cpu().numpy()
+    for r in (0, 1, 1777, 4095):
+        st, want = oracle.quant_gemm(ah[r:r + 1], bh, float_fmt(8, 7), float_fmt(8, 7),
+                                     row_base=r)
+        assert np.array_equal(bits(c[r:r + 1]), bits(want)), r
+
+
+def test_matmul_q_vs_reference_goldens(q, oracle):
+    z = golden_cases.load()
+    a, b = z["mm_a"], z["mm_b"]
+    ident = q.QuantSpec(q.FloatFormat(8, 23))
+    assert np.array_equal(bits(q.quantized_matmul(dev(a), dev(b), ident).cpu().numpy()),
+                          bits(z["mm_c"]))
+    s = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 11, 3)
+    got = q.quantized_matmul(dev(a), dev(b), s).cpu().numpy()
+    assert np.array_equal(bits(got), bits(z["qmm_fixed84_stoch_s11_c3"]))
+    assert s.call_counter == 4
+    s = q.QuantSpec(q.FloatFormat(5, 2))
+    got = q.quantized_matmul(a, b, s)  # host path
+    assert np.array_equal(bits(got), bits(z["qmm_float52_even"]))
+
+
+@pytest.mark.parametrize("M,N,K", [(100, 90, 513), (256, 128, 64), (3, 5, 7)])
+def test_matmul_q_vs_oracle(q, oracle, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    c = oracle.matmul(a, b)
+    for fmt, qf in [(fixed_fmt(8, 4), q.FixedFormat(8, 4)), (float_fmt(5, 2), q.FloatFormat(5, 2))]:
+        for mode in ALL_MODES:
+            st, want = oracle.quantize(c, fmt, mode, seed=3, call=1)
+            got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(qf, q.RoundingMode(mode), 3), 1)
+            assert np.array_equal(bits(got.cpu().numpy()), bits(want)), (fmt, mode)
+    from oracle_lib import block_fmt
+    st, want = oracle.quantize(c, block_fmt(8, 0), NEAREST_EVEN)
+    got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(q.BlockFloatFormat(8, 0)), 0)
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))

@@ -1,0 +1,302 @@
+"""GPU parity: the sm_100a quantizer kernels through the C ABI vs the oracle.
+
+Bar: bit-exact (memcmp of the fp32 bit patterns) for every format and all
+four rounding modes, stochastic included (the kernels draw the reference's
+own variates).  Checked against (a) the reference library's own outputs
+(tests/golden fixtures), (b) the C restatement on seeded inputs of assorted
+shapes, alignments and block plans, and (c) at BASELINE sizes, on sampled
+windows plus size-independent properties.
+"""
+import numpy as np
+import pytest
+
+import golden_cases
+from oracle_lib import (ALL_MODES, NEAREST_EVEN, STOCHASTIC, block_fmt, bits,
+                        fixed_fmt, float_fmt)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1910_04540_b200 as q
+    return q
+
+
+def spec_of(q, fmt, mode, seed=0):
+    if fmt.kind == 0:
+        f = q.FloatFormat(fmt.exp_bits, fmt.man_bits)
+    elif fmt.kind == 1:
+        f = q.FixedFormat(fmt.wl, fmt.fl, bool(fmt.symmetric), bool(fmt.saturate))
+    else:
+        f = q.BlockFloatFormat(fmt.wl, None if fmt.block_dim < 0 else fmt.block_dim)
+    return q.QuantSpec(f, q.RoundingMode(mode), seed, 0)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def same_bits(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return np.array_equal(bits(a), bits(b))
+
+
+# ---- (a) the reference's own outputs ---------------------------------------------
+def test_golden_fixtures_device(q):
+    n = 0
+    for i, fmt, mode, seed, call, st, x, y in golden_cases.quantize_cases():
+        spec = spec_of(q, fmt, mode, seed)
+        if st != 0:
+            with pytest.raises(q.InvalidInputError):
+                q.quantize_fused_at(dev(x), spec, call)
+            continue
+        got = q.quantize_fused_at(dev(x), spec, call)
+        assert same_bits(got, y), (i, fmt, mode)
+        n += 1
+    assert n > 300
+
+
+def test_golden_fixtures_host_path(q):
+    for i, fmt, mode, seed, call, st, x, y in golden_cases.quantize_cases():
+        if i % 3:
+            continue
+        spec = spec_of(q, fmt, mode, seed)
+        if st != 0:
+            with pytest.raises(q.InvalidInputError):
+                q.quantize_fused_at(x, spec, call)
+            continue
+        assert same_bits(q.quantize_fused_at(x, spec, call), y), (i, fmt, mode)
+
+
+def test_generators_match_reference(q):
+    z = golden_cases.load()
+    u = q.random_uniform((4097,), 7, 0, -4.0, 4.0)
+    assert same_bits(u, z["uniform_s7_m4_4"])
+    u = q.random_uniform((1000,), 2, 0, -10.0, 10.0)
+    assert same_bits(u, z["uniform_s2_m10_10"])
+    v = q.variate_tensor((1000,), 0x15EED, 0)
+    assert same_bits(v, z["variates_15eed"])
+
+
+# ---- (b) seeded inputs vs the C restatement -----------------------------------------
+ELEM_FMTS = [float_fmt(5, 2), float_fmt(8, 7), float_fmt(4, 3), float_fmt(1, 0),
+             float_fmt(8, 23), fixed_fmt(8, 4), fixed_fmt(3, 1, True),
+             fixed_fmt(6, 2, False, False), fixed_fmt(24, 100, True, False),
+             fixed_fmt(2, -126)]
+
+
+def mixed_inputs(rng, n):
+    m = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-150, 127, n)).astype(np.float32)
+    u = rng.uniform(-30, 30, n).astype(np.float32)
+    x = np.where(rng.random(n) < 0.5, m, u).astype(np.float32)
+    x[: min(n, 8)] = np.array([0.0, -0.0, 0.5, -0.5, 2.5, -2.5, 1e-45, 3.99],
+                              np.float32)[: min(n, 8)]
+    return x
+
+
+@pytest.mark.parametrize("fmt", ELEM_FMTS, ids=repr)
+@pytest.mark.parametrize("mode", ALL_MODES)
+def test_elementwise_vs_oracle_ragged(q, oracle, fmt, mode):
+    rng = np.random.default_rng(fmt.wl * 100 + fmt.exp_bits * 10 + mode)
+    spec = spec_of(q, fmt, mode, seed=1234)
+    for n in (1, 3, 4, 17, 1023, 4096 + 5, 300_001):
+        x = mixed_inputs(rng, n)
+        st, want = oracle.quantize(x, fmt, mode, seed=1234, call=n)
+        assert st == 0
+        got = q.quantize_fused_at(dev(x), spec, n)
+        assert same_bits(got, want), (fmt, mode, n)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_elementwise_misaligned_and_inplace(q, oracle, offset):
+    rng = np.random.default_rng(offset)
+    n = 100_003
+    x = mixed_inputs(rng, n)
+    fmt = fixed_fmt(8, 4)
+    st, want = oracle.quantize(x, fmt, STOCHASTIC, seed=5, call=9)
+    spec = spec_of(q, fmt, STOCHASTIC, seed=5)
+    big = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+    big[offset:offset + n] = dev(x)
+    got = q.quantize_fused_at(big[offset:offset + n], spec, 9)
+    assert same_bits(got, want)
+    # output at a different misalignment than the input: scalar path
+    out = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+    xv = big[offset:offset + n]
+    q.quantize_fused_at(xv, spec, 9, out=out[(offset + 1) % 4:(offset + 1) % 4 + n])
+    assert same_bits(out[(offset + 1) % 4:(offset + 1) % 4 + n], want)
+    # in place
+    q.quantize_fused_at(xv, spec, 9, out=xv)
+    assert same_bits(xv, want)
+
+
+BLOCK_CASES = [
+    # (shape, block_dim): covers all three plans
+    ((300, 4096), 0),       # rows in registers, 1024x4
+    ((64, 100), 0),         # rows, 128 threads
+    ((7, 20000), 0),        # rows, 1024 x 8 float4
+    ((5, 40000), 0),        # long rows -> two-pass segments
+    ((1000,), None),        # whole tensor, rows plan (1 row)
+    ((1_000_003,), None),   # whole tensor, two-pass segments, odd length
+    ((50, 70, 30), 1),      # columns plan (stride 30)
+    ((40, 33), 1),          # last dim, stride 1
+    ((3, 5, 2048), 1),      # segments with outer > 1
+    ((6, 5, 9), 2),
+    ((1, 3, 256), 1),       # leading 1: rows plan along dim 1
+    ((257, 3), 0),          # stride 3 (< 64): columns plan along dim 0
+]
+
+
+@pytest.mark.parametrize("shape,dim", BLOCK_CASES, ids=str)
+@pytest.mark.parametrize("mode", ALL_MODES)
+@pytest.mark.parametrize("wl", [8, 4])
+def test_block_plans_vs_oracle(q, oracle, shape, dim, mode, wl):
+    rng = np.random.default_rng(hash((shape, dim, mode, wl)) % 2**32)
+    x = rng.uniform(-1, 1, shape).astype(np.float32)
+    # per-slice exponents that vary, and some all-zero slices
+    if dim is not None:
+        sl = [slice(None)] * len(shape)
+        for b in range(shape[dim]):
+            sl[dim] = b
+            x[tuple(sl)] *= np.float32(2.0 ** int(rng.integers(-30, 30)))
+        sl[dim] = 0
+        x[tuple(sl)] = 0.0
+    fmt = block_fmt(wl, dim)
+    st, want = oracle.quantize(x, fmt, mode, seed=77, call=3)
+    assert st == 0
+    got = q.quantize_fused_at(dev(x), spec_of(q, fmt, mode, seed=77), 3)
+    assert same_bits(got, want), (shape, dim, mode, wl)
+    # host path (streamed rows / resident two-pass)
+    got_h = q.quantize_fused_at(x, spec_of(q, fmt, mode, seed=77), 3)
+    assert same_bits(got_h, want)
+
+
+def test_block_tiny_and_huge_maxima(q, oracle):
+    rng = np.random.default_rng(3)
+    for e in (-149, -140, -126, 0, 100, 126):
+        x = (rng.uniform(-1, 1, (16, 256)) * 2.0**e).astype(np.float32)
+        for mode in ALL_MODES:
+            fmt = block_fmt(8, 0)
+            st, want = oracle.quantize(x, fmt, mode, seed=1, call=e & 0xFF)
+            got = q.quantize_fused_at(dev(x), spec_of(q, fmt, mode, seed=1), e & 0xFF)
+            assert st == 0 and same_bits(got, want), (e, mode)
+
+
+# ---- errors (errors.hpp taxonomy) ---------------------------------------------------
+def test_errors(q):
+    spec = q.QuantSpec(q.FixedFormat(8, 4))
+    bad = np.array([1.0, np.inf, 2.0], np.float32)
+    with pytest.raises(q.InvalidInputError):
+        q.quantize_fused(dev(bad), spec)
+    with pytest.raises(q.InvalidInputError):
+        q.quantize_fused(bad, spec)
+    with pytest.raises(q.InvalidInputError):
+        q.quantize_fused(dev(np.array([np.nan, 1.0], np.float32)),
+                         q.QuantSpec(q.FloatFormat(5, 2)))
+    with pytest.raises(q.InvalidInputError):  # block max >= 2^127
+        q.quantize_fused(dev(np.array([1.0, 2.0**127], np.float32)),
+                         q.QuantSpec(q.BlockFloatFormat(8)))
+    with pytest.raises(q.ShapeError):
+        q.quantize_fused(dev(np.ones((4, 4), np.float32)),
+                         q.QuantSpec(q.BlockFloatFormat(8, 3)))
+    with pytest.raises(q.FormatError):
+        q.quantize_fused(dev(np.ones(4, np.float32)), q.QuantSpec(q.FixedFormat(1, 0)))
+    # the status word is cleared: a good call afterwards succeeds
+    q.quantize_fused(dev(np.ones(4, np.float32)), spec)
+
+
+def test_call_counter_and_replay(q):
+    # quant_ops.cpp:179-183, test_quant_ops.cpp:96-117
+    t = dev(np.random.default_rng(61).uniform(-2, 2, 100).astype(np.float32))
+    a = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 5, 0)
+    b = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 5, 0)
+    assert same_bits(q.quantize_fused(t, a), q.quantize_fused(t, b).cpu().numpy())
+    assert a.call_counter == 1
+    assert same_bits(q.quantize_fused(t, a), q.quantize_fused(t, b).cpu().numpy())
+    assert a.call_counter == 2
+    n = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.NearestEven, 1, 0)
+    q.quantize_fused(t, n)
+    assert n.call_counter == 0
+
+
+def test_pass_count_contract(q):
+    # test_quant_ops.cpp:156-181: fused <= 2 passes
+    t = dev(np.random.default_rng(71).uniform(-4, 4, (32, 32)).astype(np.float32))
+    for fmt, passes in [(q.FixedFormat(8, 4), 1), (q.FloatFormat(5, 2), 1),
+                        (q.BlockFloatFormat(8, 0), 1), (q.BlockFloatFormat(8), 2)]:
+        q.reset_pass_count()
+        q.quantize_fused_at(t, q.QuantSpec(fmt, q.RoundingMode.Stochastic), 0)
+        assert q.pass_count() == passes <= 2
+
+
+def test_identity_format_and_quantized_op(q):
+    t = dev(np.random.default_rng(41).uniform(-100, 100, (17, 9)).astype(np.float32))
+    assert same_bits(q.quantize_fused(t, q.QuantSpec(q.FloatFormat(8, 23))), t.cpu().numpy())
+    f31 = q.QuantSpec(q.FixedFormat(3, 1))
+    qrelu = q.quantized_op(torch.relu, f31)
+    r = qrelu(dev(np.array([-1.0, 0.74], np.float32))).cpu().numpy()
+    assert list(r) == [0.0, 0.5]
+
+
+def test_shards_equal_whole(q):
+    # index_base makes a sharded quantization bit-identical to the whole
+    x = q.random_uniform((1_000_000,), 2, 0, -10.0, 10.0)
+    spec = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 0x15EED)
+    whole = q.quantize_fused_at(x, spec, 0)
+    parts = []
+    for r in range(4):
+        lo, hi = r * 250_000, (r + 1) * 250_000
+        parts.append(q.quantize_fused_at(x[lo:hi], spec, 0, index_base=lo))
+    assert torch.equal(torch.cat(parts).view(torch.int32), whole.view(torch.int32))
+
+
+# ---- (c) BASELINE sizes --------------------------------------------------------------
+def test_c1_float52_16M_full(q, oracle):
+    n = 1 << 24
+    x = q.random_uniform((n,), 7, 0, -4.0, 4.0)
+    xh = x.cpu().numpy()
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        spec = q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode(mode), 0x15EED)
+        got = q.quantize_fused_at(x, spec, 0).cpu().numpy()
+        st, want = oracle.quantize(xh, float_fmt(5, 2), mode, seed=0x15EED, call=0)
+        assert st == 0 and np.array_equal(bits(got), bits(want))
+
+
+def test_c2_fixed84_1G_windows(q, oracle):
+    n = 1 << 30
+    x = q.random_uniform((n,), 2, 0, -10.0, 10.0)
+    spec = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 0x15EED)
+    y = q.quantize_fused_at(x, spec, 0)
+    w = 1 << 20
+    for lo in (0, n // 2 - 12345, n - w):
+        xs = oracle.random_uniform(w, 2, 0, -10.0, 10.0, index_base=lo)
+        assert np.array_equal(bits(xs), bits(x[lo:lo + w].cpu().numpy()))
+        st, want = oracle.quantize(xs, fixed_fmt(8, 4), STOCHASTIC, seed=0x15EED,
+                                   call=0, index_base=lo)
+        assert np.array_equal(bits(y[lo:lo + w].cpu().numpy()), bits(want)), lo
+    # properties over the whole 1G output: on the 1/16 grid and within range
+    k = y * 16.0
+    assert torch.equal(k, torch.round(k))
+    assert float(y.min()) >= -8.0 and float(y.max()) <= 7.9375
+    del x, y
+
+
+def test_c3_block_rows_65536x4096(q, oracle):
+    R, L = 65536, 4096
+    base = q.random_uniform((R, L), 3, 0, -1.0, 1.0)
+    scale = torch.exp2(torch.randint(-20, 21, (R, 1), device="cuda",
+                                     generator=torch.Generator("cuda").manual_seed(0)).float())
+    x = base * scale
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        spec = q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode(mode), 0x15EED)
+        y = q.quantize_fused_at(x, spec, 0)
+        rows = list(range(0, R, R // 32)) + [R - 1]
+        for r in rows:
+            st, want = oracle.quantize(x[r].cpu().numpy(), block_fmt(8),
+                                       mode, seed=0x15EED, call=0, index_base=r * L)
+            assert np.array_equal(bits(y[r].cpu().numpy()), bits(want)), (mode, r)
+        if mode == NEAREST_EVEN:  # idempotence over all 2^28 elements
+            y2 = q.quantize_fused_at(y, spec, 0)
+            assert torch.equal(y2.view(torch.int32), y.view(torch.int32))
