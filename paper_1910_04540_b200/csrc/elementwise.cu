@@ -23,11 +23,12 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
 
+template <bool TINY>
 struct FixedSatOp {
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
-    return quant_fixed<M, true>(x, p, v);
+    return quant_fixed<M, true, TINY>(x, p, v);
   }
 };
 struct FixedWrapOp {
@@ -45,18 +46,22 @@ struct FloatOp {
   }
 };
 
+// z = key ^ flat_index.  Non-finite inputs are not special-cased per
+// element: the kernel folds |x| bits into a running maximum and flags the
+// call (the reference throws and discards the whole output,
+// quant_ops.cpp:21-29), so the output of such a call is unspecified.
 template <int M, class Op>
-__device__ __forceinline__ float qelem(const Op& op, float x, uint64_t key,
-                                       uint64_t idx, uint32_t& bad) {
+__device__ __forceinline__ float qelem(const Op& op, float x, uint64_t z,
+                                       uint32_t& amax) {
   uint32_t v = 0;
-  if (M == kStochastic) v = variate24(key, idx);
-  const bool nf = nonfinite(x);
-  bad |= nf ? 1u : 0u;
-  const float q = op.template apply<M>(x, v);
-  return nf ? 0.0f : q;  // quant_ops.cpp:21-25: non-finite writes 0
+  if (M == kStochastic) v = variate24_z(z);
+  amax = max(amax, f2u(x) & 0x7FFFFFFFu);
+  return op.template apply<M>(x, v);
 }
 
-template <int M, class Op>
+// IDX4: (base + head) % 4 == 0, so the four flat indices of a float4 differ
+// from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
+template <int M, class Op, bool IDX4>
 __global__ void __launch_bounds__(kThreads)
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
@@ -64,7 +69,7 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t n4 = (n - head) >> 2;
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
-  uint32_t bad = 0;
+  uint32_t amax = 0;
   const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
   for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
        i0 < n4; i0 += step) {
@@ -79,11 +84,23 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t j = i0 + (int64_t)u * kThreads;
       if (j < n4) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
+        uint64_t z0, z1, z2, z3;
+        if (IDX4) {
+          z0 = key ^ idx;
+          z1 = z0 ^ 1u;
+          z2 = z0 ^ 2u;
+          z3 = z0 ^ 3u;
+        } else {
+          z0 = key ^ idx;
+          z1 = key ^ (idx + 1);
+          z2 = key ^ (idx + 2);
+          z3 = key ^ (idx + 3);
+        }
         float4 o;
-        o.x = qelem<M>(op, v[u].x, key, idx, bad);
-        o.y = qelem<M>(op, v[u].y, key, idx + 1, bad);
-        o.z = qelem<M>(op, v[u].z, key, idx + 2, bad);
-        o.w = qelem<M>(op, v[u].w, key, idx + 3, bad);
+        o.x = qelem<M>(op, v[u].x, z0, amax);
+        o.y = qelem<M>(op, v[u].y, z1, amax);
+        o.z = qelem<M>(op, v[u].z, z2, amax);
+        o.w = qelem<M>(op, v[u].w, z3, amax);
         __stcs(y4 + j, o);
       }
     }
@@ -94,9 +111,9 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < extra;
        t += (int64_t)gridDim.x * kThreads) {
     const int64_t e = t < head ? t : tail0 + (t - head);
-    y[e] = qelem<M>(op, x[e], key, base + (uint64_t)e, bad);
+    y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), amax);
   }
-  if (__any_sync(0xFFFFFFFFu, bad != 0) && (threadIdx.x & 31) == 0)
+  if (__any_sync(0xFFFFFFFFu, amax >= 0x7F800000u) && (threadIdx.x & 31) == 0)
     atomicOr(status, kStatusNonFinite);
 }
 
@@ -117,15 +134,24 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   const int64_t n4 = (n - head) >> 2;
   const int64_t work = std::max<int64_t>(n4, n - 4 * n4);
   const DeviceInfo& di = device_info();
+  const bool idx4 = ((base + (uint64_t)head) & 3u) == 0;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_elementwise<M, Op>,
-                                                kThreads, 0);
+  if (idx4)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_elementwise<M, Op, true>, kThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_elementwise<M, Op, false>, kThreads, 0);
   const int64_t cap = (int64_t)di.sm_count * std::max(per_sm, 1);
   const int64_t want = (work + (int64_t)kThreads * kUnroll - 1) /
                        ((int64_t)kThreads * kUnroll);
   const int grid = (int)std::max<int64_t>(1, std::min(cap, want));
-  k_elementwise<M, Op><<<grid, kThreads, 0, s>>>(x, y, n, head, base, key, op,
-                                                 status);
+  if (idx4)
+    k_elementwise<M, Op, true><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
+                                                         key, op, status);
+  else
+    k_elementwise<M, Op, false><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
+                                                          key, op, status);
   note_launch();
   return cudaGetLastError();
 }
@@ -173,8 +199,10 @@ int gen_grid(int64_t n) {
 cudaError_t launch_fixed(const float* x, float* y, int64_t n, uint64_t base,
                          uint64_t key, const FixedParams& p, int mode,
                          uint32_t* status, cudaStream_t s) {
+  if (p.saturate && !p.tiny)
+    return dispatch_mode(x, y, n, base, key, FixedSatOp<false>{p}, mode, status, s);
   if (p.saturate)
-    return dispatch_mode(x, y, n, base, key, FixedSatOp{p}, mode, status, s);
+    return dispatch_mode(x, y, n, base, key, FixedSatOp<true>{p}, mode, status, s);
   return dispatch_mode(x, y, n, base, key, FixedWrapOp{p}, mode, status, s);
 }
 

@@ -94,8 +94,10 @@ LPQ_HD uint64_t stream_key(uint64_t seed, uint64_t call) {
 // (rng.hpp:34-36).  Kernels keep it as the 24-bit integer v, u = v * 2^-24.
 // (z ^ (z >> 31)) >> 40 == z >> 40, so the final xor-shift of the splitmix
 // finalizer is dropped, and only the high word of the last product is formed.
-LPQ_HD uint32_t variate24(uint64_t key, uint64_t index) {
-  uint64_t z = (key ^ index) + 0x9E3779B97F4A7C15ull;
+// z = key ^ index (callers that know index % 4 == 0 form key ^ (index + q)
+// as (key ^ index) ^ q without a 64-bit add).
+LPQ_HD uint32_t variate24_z(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = z ^ (z >> 27);
   const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
@@ -107,6 +109,10 @@ LPQ_HD uint32_t variate24(uint64_t key, uint64_t index) {
       (uint32_t)(((uint64_t)lo * c_lo) >> 32) + lo * c_hi + hi * c_lo;
 #endif
   return top >> 8;
+}
+
+LPQ_HD uint32_t variate24(uint64_t key, uint64_t index) {
+  return variate24_z(key ^ index);
 }
 
 LPQ_HD float variate_float(uint32_t v) { return (float)v * 0x1p-24f; }
@@ -125,7 +131,7 @@ LPQ_HD float variate_float(uint32_t v) { return (float)v * 0x1p-24f; }
 // (fa > 0 && u >= 1 - fa) = fl(a) + (fa >= 1 - u), since 1 - u > 0.  fa =
 // a - floor(a) is exact for a >= 0, and 1 - u is exact (u on the 2^-24 grid),
 // so both compares are exact -- unlike r - floor(r) in fp32 for r in (-1,0).
-template <int M>
+template <int M, bool TINY = true>
 LPQ_HD float round_mag(float a, bool neg, bool xnz, uint32_t v) {
   if (M == kNearestEven) {
 #if defined(__CUDA_ARCH__)
@@ -142,13 +148,13 @@ LPQ_HD float round_mag(float a, bool neg, bool xnz, uint32_t v) {
   } else if (M == kNearestZero) {
     up = fa > 0.5f;
   } else {
+    // branch-free: r >= 0 compares fa > u, r < 0 compares fa >= 1 - u.
+    // a == 0 with x != 0 and r > 0: the true fraction is in (0, 2^-150], so
+    // u < it iff u == 0.
     const float u = variate_float(v);
-    if (neg) {
-      up = fa >= fsub(1.0f, u);
-    } else {
-      // a == 0 with x != 0: true fraction is in (0, 2^-150]; u < it iff u == 0
-      up = (fa > u) | ((a == 0.0f) & xnz & (v == 0u));
-    }
+    const float thr = neg ? fsub(1.0f, u) : u;
+    up = (fa > thr) | (neg & (fa == thr));
+    if (TINY) up |= !neg & (a == 0.0f) & xnz & (v == 0u);
   }
   return up ? fadd(qa, 1.0f) : qa;
 }
@@ -175,6 +181,7 @@ struct FixedParams {
   int32_t half;    // 2^(wl-1)
   int32_t wl;
   int32_t saturate;
+  int32_t tiny;    // fl <= -1: x * 2^fl may flush to zero
 };
 
 LPQ_HD FixedParams make_fixed(int wl, int fl, bool symmetric, bool saturate) {
@@ -189,16 +196,18 @@ LPQ_HD FixedParams make_fixed(int wl, int fl, bool symmetric, bool saturate) {
   p.half = 1 << (wl - 1);
   p.wl = wl;
   p.saturate = saturate ? 1 : 0;
+  p.tiny = fl <= -1 ? 1 : 0;
   return p;
 }
 
-template <int M, bool SAT>
+// TINY: fl <= -1, where x * 2^fl can flush to zero (make_fixed: p.tiny).
+template <int M, bool SAT, bool TINY = true>
 LPQ_HD float quant_fixed(float x, const FixedParams& p, uint32_t v) {
   const float r = fmul(x, p.up);
   const float a = fabsf(r);
   const bool neg = x < 0.0f;
   const bool xnz = x != 0.0f;
-  const float kmag = round_mag<M>(a, neg, xnz, v);
+  const float kmag = round_mag<M, TINY>(a, neg, xnz, v);
   const bool kneg = (kmag == 0.0f) ? zero_negative<M>(neg) : neg;
   if (SAT) {
     float k = kneg ? -kmag : kmag;
@@ -258,26 +267,28 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
 
 template <int M>
 LPQ_HD float quant_float(float x, const FloatParams& p, uint32_t v) {
+  // Branch-free: one rounding of either the in-range significand
+  // r = |x| * 2^(man - e) in [2^man, 2^(man+1)) (same mantissa bits, new
+  // exponent) or, below 2^min_exp, of |x| * 2^-min_exp < 1 over {0, 1}.
   const uint32_t xb = f2u(x);
   const uint32_t ab = xb & 0x7FFFFFFFu;
-  if (ab == 0u) return x;  // zero passes through with its sign
   const bool neg = (int32_t)xb < 0;
   const int e = (int)(ab >> 23) - 127;  // denormals give -127 < min_exp
-  if (e > p.max_exp) return neg ? -p.max_value : p.max_value;
-  if (e >= p.min_exp) {
-    // r = |x| * 2^(man - e) in [2^man, 2^(man+1)): same mantissa, new exponent
-    const float r = u2f((ab & 0x7FFFFFu) | p.r_exp);
-    const float k = round_mag<M>(r, neg, true, v);
-    if (e == p.max_exp && k >= p.carry) return neg ? -p.max_value : p.max_value;
-    // q = k * 2^(e - man): exponent-field add (k >= 1, q normal)
-    const float q = u2f(f2u(k) + ((uint32_t)(e - p.man) << 23));
-    return neg ? -q : q;
-  }
-  // underflow: round |x| / 2^min_exp < 1 over {0, 2^min_exp}
-  const float a = fmul(u2f(ab), p.under_up);
-  const float k = round_mag<M>(a, neg, true, v);
-  if (k == 0.0f) return zero_negative<M>(neg) ? -0.0f : 0.0f;
-  return neg ? -p.under_down : p.under_down;
+  const bool under = e < p.min_exp;
+  const float r_in = u2f((ab & 0x7FFFFFu) | p.r_exp);
+  const float r_un = fmul(u2f(ab), p.under_up);
+  const float k = round_mag<M>(under ? r_un : r_in, neg, true, v);
+  // q = k * 2^(e - man) (or k * 2^min_exp): exponent-field add, k >= 1
+  const int sh = under ? p.min_exp : e - p.man;
+  uint32_t qb = f2u(k) + ((uint32_t)sh << 23);
+  const bool kz = k == 0.0f;
+  if (kz) qb = 0u;
+  // saturation: beyond the top binade, or a carry out of it
+  const bool sat = (e > p.max_exp) | ((e == p.max_exp) & (k >= p.carry));
+  if (sat) qb = f2u(p.max_value);
+  const bool kneg = kz ? zero_negative<M>(neg) : neg;
+  if (kneg) qb |= 0x80000000u;
+  return ab == 0u ? x : u2f(qb);  // zero passes through with its sign
 }
 
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;

@@ -17,7 +17,11 @@ void run(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f) {
     for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float<M>(x[i], p, v ? v[i] : 0u);
   } else if (f->saturate) {
     const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, true);
-    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true>(x[i], p, v ? v[i] : 0u);
+    // the kernels' dispatch: the underflow guard only when fl <= -1
+    if (p.tiny)
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true, true>(x[i], p, v ? v[i] : 0u);
+    else
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true, false>(x[i], p, v ? v[i] : 0u);
   } else {
     const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, false);
     for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, false>(x[i], p, v ? v[i] : 0u);

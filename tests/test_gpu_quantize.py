@@ -222,13 +222,17 @@ def test_call_counter_and_replay(q):
 
 
 def test_pass_count_contract(q):
-    # test_quant_ops.cpp:156-181: fused <= 2 passes
-    t = dev(np.random.default_rng(71).uniform(-4, 4, (32, 32)).astype(np.float32))
-    for fmt, passes in [(q.FixedFormat(8, 4), 1), (q.FloatFormat(5, 2), 1),
-                        (q.BlockFloatFormat(8, 0), 1), (q.BlockFloatFormat(8), 2)]:
+    # test_quant_ops.cpp:156-181: fused <= 2 data passes; ours counts the
+    # HBM passes it actually makes (1, or 2 for the two-pass block plans)
+    rng = np.random.default_rng(71)
+    cases = [(q.FixedFormat(8, 4), (32, 32), 1), (q.FloatFormat(5, 2), (32, 32), 1),
+             (q.BlockFloatFormat(8, 0), (16, 256), 1), (q.BlockFloatFormat(8), (32, 32), 1),
+             (q.BlockFloatFormat(8), (8, 40000), 2), (q.BlockFloatFormat(8, 1), (32, 32), 2)]
+    for fmt, shape, passes in cases:
+        t = dev(rng.uniform(-4, 4, shape).astype(np.float32))
         q.reset_pass_count()
         q.quantize_fused_at(t, q.QuantSpec(fmt, q.RoundingMode.Stochastic), 0)
-        assert q.pass_count() == passes <= 2
+        assert q.pass_count() == passes <= 2, (fmt, shape)
 
 
 def test_identity_format_and_quantized_op(q):
