@@ -95,7 +95,7 @@ def build_host_math(force=False, verbose=False):
     if force or _newer(HOST_MATH, [src, os.path.join(CSRC, "quant_math.cuh")]):
         cxx = shutil.which("g++") or "g++"
         _run([cxx, "-std=c++17", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
-              "-fno-fast-math", "-o", HOST_MATH, src], verbose)
+              "-fno-fast-math", "-frounding-math", "-o", HOST_MATH, src], verbose)
     return HOST_MATH
 
 

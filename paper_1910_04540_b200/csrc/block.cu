@@ -40,25 +40,33 @@ __device__ __forceinline__ uint32_t nf4(const float4& v) {
              ? 1u : 0u;
 }
 
-template <int M>
+// TWO: the block's scales need two factors (maxima near the fp32 range
+// ends); uniform per block, so kernels branch once per block/row.
+template <int M, bool TWO>
 __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
                                     float kmax, uint64_t key, uint64_t idx) {
   uint32_t v = 0;
   if (M == kStochastic) v = variate24(key, idx);
-  const float q = quant_block<M>(x, s, kmin, kmax, v);
-  return nonfinite(x) ? 0.0f : q;
+  if (M == kNearestEven || M == kStochastic)
+    return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
+        x, s, kmin, kmax, v);
+  return quant_block<M>(x, s, kmin, kmax, v);
 }
 
-template <int M>
+template <int M, bool TWO>
 __device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
                                       float kmin, float kmax, uint64_t key,
                                       uint64_t idx) {
   float4 o;
-  o.x = qb<M>(x.x, s, kmin, kmax, key, idx);
-  o.y = qb<M>(x.y, s, kmin, kmax, key, idx + 1);
-  o.z = qb<M>(x.z, s, kmin, kmax, key, idx + 2);
-  o.w = qb<M>(x.w, s, kmin, kmax, key, idx + 3);
+  o.x = qb<M, TWO>(x.x, s, kmin, kmax, key, idx);
+  o.y = qb<M, TWO>(x.y, s, kmin, kmax, key, idx + 1);
+  o.z = qb<M, TWO>(x.z, s, kmin, kmax, key, idx + 2);
+  o.w = qb<M, TWO>(x.w, s, kmin, kmax, key, idx + 3);
   return o;
+}
+
+__device__ __forceinline__ bool two_factor(const BlockScale& s) {
+  return s.s2 != 1.0f || s.o2 != 1.0f;
 }
 
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t bits) {
@@ -106,11 +114,20 @@ __global__ void __launch_bounds__(T)
     const BlockScale sc = make_block_scale(row_max, wl);
     if (sc.bad) bad |= 2u;
     const uint64_t row_base = base + (uint64_t)(r * L);
+    if (!two_factor(sc)) {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int64_t j = threadIdx.x + (int64_t)k * T;
-      if (j < L4)
-        __stcs(yr + j, qb4<M>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+      for (int k = 0; k < VPT; ++k) {
+        const int64_t j = threadIdx.x + (int64_t)k * T;
+        if (j < L4)
+          __stcs(yr + j, qb4<M, false>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const int64_t j = threadIdx.x + (int64_t)k * T;
+        if (j < L4)
+          __stcs(yr + j, qb4<M, true>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+      }
     }
     __syncthreads();  // red/row_max are reused by the next row
   }
@@ -217,20 +234,22 @@ __global__ void __launch_bounds__(kSegT)
         const int j = threadIdx.x + k * kSegT;
         if (4 * j < len) v[k] = __ldcs(x4 + j);
       }
+      const bool two = two_factor(sc);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int j = threadIdx.x + k * kSegT;
         if (4 * j < len) {
           bad |= nf4(v[k]);
-          __stcs(y4 + j, qb4<M>(v[k], sc, kmin, kmax, key,
-                                base + (uint64_t)(e0 + 4 * j)));
+          const uint64_t idx = base + (uint64_t)(e0 + 4 * j);
+          __stcs(y4 + j, two ? qb4<M, true>(v[k], sc, kmin, kmax, key, idx)
+                             : qb4<M, false>(v[k], sc, kmin, kmax, key, idx));
         }
       }
     } else {
       for (int j = threadIdx.x; j < len; j += kSegT) {
         const float xv = x[e0 + j];
         bad |= nonfinite(xv) ? 1u : 0u;
-        y[e0 + j] = qb<M>(xv, sc, kmin, kmax, key, base + (uint64_t)(e0 + j));
+        y[e0 + j] = qb<M, true>(xv, sc, kmin, kmax, key, base + (uint64_t)(e0 + j));
       }
     }
   }
@@ -315,10 +334,10 @@ __global__ void __launch_bounds__(kColT)
       const float4 v = load4<VEC>(x + r * W, c, W);
       const uint64_t idx = base + (uint64_t)(r * W + c);
       float4 o;
-      o.x = qb<M>(v.x, s[0], kmin, kmax, key, idx);
-      o.y = qb<M>(v.y, s[1], kmin, kmax, key, idx + 1);
-      o.z = qb<M>(v.z, s[2], kmin, kmax, key, idx + 2);
-      o.w = qb<M>(v.w, s[3], kmin, kmax, key, idx + 3);
+      o.x = qb<M, true>(v.x, s[0], kmin, kmax, key, idx);
+      o.y = qb<M, true>(v.y, s[1], kmin, kmax, key, idx + 1);
+      o.z = qb<M, true>(v.z, s[2], kmin, kmax, key, idx + 2);
+      o.w = qb<M, true>(v.w, s[3], kmin, kmax, key, idx + 3);
       if (VEC) {
         bad |= nf4(v);
         __stcs(reinterpret_cast<float4*>(y + r * W + c), o);

@@ -28,7 +28,8 @@ struct FixedSatOp {
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
-    return quant_fixed<M, true, TINY>(x, p, v);
+    if (TINY) return quant_fixed<M, true, true>(x, p, v);
+    return quant_fixed_sat_fast<M>(x, p, v);
   }
 };
 struct FixedWrapOp {
@@ -38,10 +39,14 @@ struct FixedWrapOp {
     return quant_fixed<M, false>(x, p, v);
   }
 };
+// FAST: the streaming form (even/stochastic, exp_bits >= 2)
+template <bool FAST>
 struct FloatOp {
   FloatParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
+    if (FAST && (M == kNearestEven || M == kStochastic))
+      return quant_float_fast<M == kNearestEven ? kNearestEven : kStochastic>(x, p, v);
     return quant_float<M>(x, p, v);
   }
 };
@@ -50,12 +55,14 @@ struct FloatOp {
 // element: the kernel folds |x| bits into a running maximum and flags the
 // call (the reference throws and discards the whole output,
 // quant_ops.cpp:21-29), so the output of such a call is unspecified.
+// nf accumulates x * 0 + nf on the FMA pipe: it stays +0 for finite x and
+// turns NaN for any +-inf or NaN.
 template <int M, class Op>
 __device__ __forceinline__ float qelem(const Op& op, float x, uint64_t z,
-                                       uint32_t& amax) {
+                                       uint32_t m32, float& nf) {
   uint32_t v = 0;
-  if (M == kStochastic) v = variate24_z(z);
-  amax = max(amax, f2u(x) & 0x7FFFFFFFu);
+  if (M == kStochastic) v = variate24_zb(z, m32);
+  nf = __fmaf_rn(x, 0.0f, nf);
   return op.template apply<M>(x, v);
 }
 
@@ -65,11 +72,11 @@ template <int M, class Op, bool IDX4>
 __global__ void __launch_bounds__(kThreads)
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
-                  uint32_t* __restrict__ status) {
+                  uint32_t m32, uint32_t* __restrict__ status) {
   const int64_t n4 = (n - head) >> 2;
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
-  uint32_t amax = 0;
+  float nf = 0.0f;
   const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
   for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
        i0 < n4; i0 += step) {
@@ -97,10 +104,10 @@ __global__ void __launch_bounds__(kThreads)
           z3 = key ^ (idx + 3);
         }
         float4 o;
-        o.x = qelem<M>(op, v[u].x, z0, amax);
-        o.y = qelem<M>(op, v[u].y, z1, amax);
-        o.z = qelem<M>(op, v[u].z, z2, amax);
-        o.w = qelem<M>(op, v[u].w, z3, amax);
+        o.x = qelem<M>(op, v[u].x, z0, m32, nf);
+        o.y = qelem<M>(op, v[u].y, z1, m32, nf);
+        o.z = qelem<M>(op, v[u].z, z2, m32, nf);
+        o.w = qelem<M>(op, v[u].w, z3, m32, nf);
         __stcs(y4 + j, o);
       }
     }
@@ -111,9 +118,9 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < extra;
        t += (int64_t)gridDim.x * kThreads) {
     const int64_t e = t < head ? t : tail0 + (t - head);
-    y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), amax);
+    y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), m32, nf);
   }
-  if (__any_sync(0xFFFFFFFFu, amax >= 0x7F800000u) && (threadIdx.x & 31) == 0)
+  if (__any_sync(0xFFFFFFFFu, nf != nf) && (threadIdx.x & 31) == 0)
     atomicOr(status, kStatusNonFinite);
 }
 
@@ -148,10 +155,10 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   const int grid = (int)std::max<int64_t>(1, std::min(cap, want));
   if (idx4)
     k_elementwise<M, Op, true><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                         key, op, status);
+                                                         key, op, 32u, status);
   else
     k_elementwise<M, Op, false><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                          key, op, status);
+                                                          key, op, 32u, status);
   note_launch();
   return cudaGetLastError();
 }
@@ -209,7 +216,9 @@ cudaError_t launch_fixed(const float* x, float* y, int64_t n, uint64_t base,
 cudaError_t launch_float(const float* x, float* y, int64_t n, uint64_t base,
                          uint64_t key, const FloatParams& p, int mode,
                          uint32_t* status, cudaStream_t s) {
-  return dispatch_mode(x, y, n, base, key, FloatOp{p}, mode, status, s);
+  if (!p.tiny)
+    return dispatch_mode(x, y, n, base, key, FloatOp<true>{p}, mode, status, s);
+  return dispatch_mode(x, y, n, base, key, FloatOp<false>{p}, mode, status, s);
 }
 
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,

@@ -17,6 +17,9 @@
 #include <stdint.h>
 #include <string.h>
 #include <math.h>
+#if !defined(__CUDA_ARCH__)
+#include <fenv.h>
+#endif
 
 #if defined(__CUDACC__)
 #define LPQ_HD __host__ __device__ __forceinline__
@@ -77,6 +80,46 @@ LPQ_HD float fsub(float a, float b) {
 #endif
 }
 
+// u * 2^-24 - r rounded toward -inf, i.e. FFMA.RM(v, 2^-24, -r): one
+// directed rounding of the exact value (v * 2^-24 is exact).
+LPQ_HD float fma_rd_variate(uint32_t v, float r) {
+#if defined(__CUDA_ARCH__)
+  return __fmaf_rd(__uint2float_rn(v), 0x1p-24f, -r);
+#else
+  const int old = fegetround();
+  fesetround(FE_DOWNWARD);
+  volatile float vf = (float)v;
+  volatile float out = fmaf(vf, 0x1p-24f, -r);
+  fesetround(old);
+  return out;
+#endif
+}
+
+LPQ_HD float rint_f(float a) {
+#if defined(__CUDA_ARCH__)
+  return rintf(a);
+#else
+  return nearbyintf(a);
+#endif
+}
+
+// Signed integer rounding of r for the two modes the streaming kernels
+// specialise (rounding.hpp:27-37, 56-59):
+//   NearestEven: rint(r)  (IEEE RNE; -0 may appear, callers add +0)
+//   Stochastic : floor(r) + (u < r - floor(r)) == -floor(u - r), and with
+//                s = RD(u - r) (a single round-toward-minus-infinity FFMA),
+//                floor(s) == floor(u - r) exactly: if u - r lies in
+//                (m, m + 1) for an integer m, RD keeps it in [m, m + 1)
+//                because m is representable (|r| < 2^24 -- beyond that r is
+//                an integer and RD(u - r) == -r).  One FFMA + one FRND
+//                replace the fraction/compare sequence.
+// r must be exact; flushed-to-zero r is the caller's business (see TINY).
+template <int M>
+LPQ_HD float round_signed(float r, uint32_t v) {
+  if (M == kNearestEven) return rint_f(r);
+  return -floorf(fma_rd_variate(v, r));
+}
+
 // ---- counter-based RNG: bit-identical to proj/include/lpsim/rng.hpp -------
 
 LPQ_HD uint64_t mix64(uint64_t z) {
@@ -113,6 +156,33 @@ LPQ_HD uint32_t variate24_z(uint64_t z) {
 
 LPQ_HD uint32_t variate24(uint64_t key, uint64_t index) {
   return variate24_z(key ^ index);
+}
+
+LPQ_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+// Pipe-balanced form of variate24_z for the streaming kernels (identical
+// result).  ncu showed the stochastic kernels ALU-pipe-bound (shifts, xors,
+// compares all issue to the ALU pipe, multiplies to the FMA pipe), so the
+// second xor-shift z ^= z >> 27 is formed with IMAD.HI/IMAD against the
+// runtime multiplier m32 == 32 (a kernel argument, so ptxas cannot turn the
+// multiplies back into shifts):  (z >> 27).lo = hi(lo*32) + hi*32,
+// (z >> 27).hi = hi(hi*32).
+LPQ_HD uint32_t variate24_zb(uint64_t z, uint32_t m32) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  const uint32_t slo = umulhi32(lo, m32) + hi * m32;
+  const uint32_t shi = umulhi32(hi, m32);
+  lo ^= slo;
+  hi ^= shi;
+  const uint32_t top = umulhi32(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu;
+  return top >> 8;
 }
 
 LPQ_HD float variate_float(uint32_t v) { return (float)v * 0x1p-24f; }
@@ -234,6 +304,38 @@ LPQ_HD float quant_fixed(float x, const FixedParams& p, uint32_t v) {
   return fmul((float)m, p.down);
 }
 
+LPQ_HD float fma_rn(float a, float b, float c) {
+#if defined(__CUDA_ARCH__)
+  return __fmaf_rn(a, b, c);
+#else
+  return fmaf(a, b, c);
+#endif
+}
+
+// Saturating fixed point with fl >= 0 (x * 2^fl cannot flush to zero), the
+// streaming kernels' form.  NearestEven / Stochastic round the signed value
+// directly (round_signed); the reference's +0 for a zero result comes from
+// k * 2^-fl + 0 in one FFMA.  NearestAway / NearestTowardZero keep the
+// magnitude path with the sign applied by a multiply by +-1.  Identical
+// results to quant_fixed<M, true, false>.
+template <int M>
+LPQ_HD float quant_fixed_sat_fast(float x, const FixedParams& p, uint32_t v) {
+  const float r = fmul(x, p.up);
+  if (M == kNearestEven || M == kStochastic) {
+    float k = round_signed<M>(r, v);
+    k = fminf(fmaxf(k, p.kmin), p.kmax);  // +-inf clamp too
+    return fma_rn(k, p.down, 0.0f);       // exact product; -0 + 0 = +0
+  }
+  const float a = fabsf(r);
+  const bool neg = x < 0.0f;
+  const float kmag = round_mag<M, false>(a, neg, true, v);
+  float k = fmul(kmag, neg ? -1.0f : 1.0f);  // -0 when kmag == 0 and r < 0
+  k = fminf(fmaxf(k, p.kmin), p.kmax);
+  float out = fmul(k, p.down);
+  if (M == kNearestZero && kmag == 0.0f) out = neg ? 0.0f : -0.0f;
+  return out;  // NearestAway: -0 iff r < 0, as the multiply left it
+}
+
 // ---- low-width float (FloatQuantizer, scalar_quant.hpp:103-141;
 //      fused_float, quant_ops.cpp:52-66) -------------------------------------
 
@@ -246,6 +348,7 @@ struct FloatParams {
   float under_down;  // 2^min_exp
   float carry;       // 2^(man+1)
   uint32_t r_exp;    // (man + 127) << 23
+  int32_t tiny;      // min_exp >= 1: |x| * 2^-min_exp may flush to zero
 };
 
 LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
@@ -262,6 +365,7 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.under_down = u2f((uint32_t)(127 + p.min_exp) << 23);
   p.carry = u2f((uint32_t)(127 + man_bits + 1) << 23);
   p.r_exp = (uint32_t)(man_bits + 127) << 23;
+  p.tiny = p.min_exp >= 1 ? 1 : 0;
   return p;
 }
 
@@ -289,6 +393,29 @@ LPQ_HD float quant_float(float x, const FloatParams& p, uint32_t v) {
   const bool kneg = kz ? zero_negative<M>(neg) : neg;
   if (kneg) qb |= 0x80000000u;
   return ab == 0u ? x : u2f(qb);  // zero passes through with its sign
+}
+
+// Float quantizer, streaming form for NearestEven / Stochastic when
+// |x| * 2^-min_exp cannot flush to zero (min_exp <= 0, i.e. exp_bits >= 2):
+// the signed significand r = +-|x| * 2^(man - e) (or x * 2^-min_exp below the
+// normal range) is rounded once with round_signed; identical results to
+// quant_float<M>.
+template <int M>
+LPQ_HD float quant_float_fast(float x, const FloatParams& p, uint32_t v) {
+  const uint32_t xb = f2u(x);
+  const uint32_t ab = xb & 0x7FFFFFFFu;
+  const uint32_t sign = xb & 0x80000000u;
+  const int e = (int)(ab >> 23) - 127;
+  const bool under = e < p.min_exp;
+  const float r_in = u2f((xb & 0x807FFFFFu) | p.r_exp);
+  const float r_un = fmul(x, p.under_up);
+  const float k = fabsf(round_signed<M>(under ? r_un : r_in, v));
+  const int sh = under ? p.min_exp : e - p.man;
+  uint32_t qb = (f2u(k) + ((uint32_t)sh << 23)) | sign;
+  const bool sat = (e > p.max_exp) | ((e == p.max_exp) & (k >= p.carry));
+  if (sat) qb = f2u(p.max_value) | sign;
+  if (k == 0.0f) qb = 0u;  // +0 for both modes
+  return ab == 0u ? x : u2f(qb);
 }
 
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;
@@ -347,6 +474,27 @@ LPQ_HD float quant_block(float x, const BlockScale& s, float kmin, float kmax,
   float k = kneg ? -kmag : kmag;
   k = fminf(fmaxf(k, kmin), kmax);
   return fmul(fmul(k, s.o1), s.o2);
+}
+
+// Block element, streaming form for NearestEven / Stochastic: signed
+// rounding (round_signed), k * delta + 0 in one FFMA (-0 -> +0, and a single
+// rounding of the exact k * 2^shift).  TWO: the scales needed two factors
+// (block maxima near the fp32 range ends).  A product x * 2^-shift that
+// flushed to zero is replaced by the smallest denormal with x's sign, which
+// gives the exact stochastic decision (u < |r| iff u == 0 for r > 0; never
+// for r < 0).  All-zero blocks have zero scales and produce +0.  Identical
+// results to quant_block<M>.
+template <int M, bool TWO>
+LPQ_HD float quant_block_fast(float x, const BlockScale& s, float kmin,
+                              float kmax, uint32_t v) {
+  float r = fmul(x, s.s1);
+  if (TWO) r = fmul(r, s.s2);
+  if (M == kStochastic && r == 0.0f && x != 0.0f)
+    r = x < 0.0f ? -0x1p-149f : 0x1p-149f;
+  float k = round_signed<M>(r, v);
+  k = fminf(fmaxf(k, kmin), kmax);
+  if (TWO) return fma_rn(fmul(k, s.o1), s.o2, 0.0f);
+  return fma_rn(k, s.o1, 0.0f);
 }
 
 LPQ_HD bool nonfinite(float x) { return (f2u(x) & 0x7F800000u) == 0x7F800000u; }

@@ -13,15 +13,20 @@ struct Fmt { int32_t kind, exp_bits, man_bits, wl, fl, symmetric, saturate, bloc
 template <int M>
 void run(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f) {
   if (f->kind == 0) {
+    // the kernels' dispatch: the streaming form for even/stochastic unless
+    // |x| * 2^-min_exp can flush to zero
     const lpq::FloatParams p = lpq::make_float(f->exp_bits, f->man_bits);
-    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float<M>(x[i], p, v ? v[i] : 0u);
+    if ((M == 0 || M == 1) && !p.tiny)
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float_fast<(M == 0 ? 0 : 1)>(x[i], p, v ? v[i] : 0u);
+    else
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float<M>(x[i], p, v ? v[i] : 0u);
   } else if (f->saturate) {
     const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, true);
     // the kernels' dispatch: the underflow guard only when fl <= -1
     if (p.tiny)
       for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true, true>(x[i], p, v ? v[i] : 0u);
     else
-      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, true, false>(x[i], p, v ? v[i] : 0u);
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed_sat_fast<M>(x[i], p, v ? v[i] : 0u);
   } else {
     const lpq::FixedParams p = lpq::make_fixed(f->wl, f->fl, f->symmetric, false);
     for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_fixed<M, false>(x[i], p, v ? v[i] : 0u);
@@ -34,7 +39,14 @@ void run_block(const float* x, const uint32_t* v, float* y, int64_t n, int wl,
   const lpq::BlockScale s = lpq::make_block_scale(max_bits, wl);
   *bad = s.bad;
   const float kmin = -(float)(1 << (wl - 1)), kmax = (float)((1 << (wl - 1)) - 1);
-  for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_block<M>(x[i], s, kmin, kmax, v ? v[i] : 0u);
+  const bool two = s.s2 != 1.0f || s.o2 != 1.0f;
+  // the kernels' dispatch (block.cu)
+  if ((M == 0 || M == 1) && two)
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_block_fast<(M == 0 ? 0 : 1), true>(x[i], s, kmin, kmax, v ? v[i] : 0u);
+  else if (M == 0 || M == 1)
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_block_fast<(M == 0 ? 0 : 1), false>(x[i], s, kmin, kmax, v ? v[i] : 0u);
+  else
+    for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_block<M>(x[i], s, kmin, kmax, v ? v[i] : 0u);
 }
 }  // namespace
 
@@ -63,6 +75,10 @@ int hm_quant_block(const float* x, const uint32_t* v, float* y, int64_t n, int w
 uint32_t hm_variate24(uint64_t key, uint64_t index) { return lpq::variate24(key, index); }
 void hm_variates24(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24(key, base + (uint64_t)i);
+}
+// the kernels' pipe-balanced form (must equal variate24)
+void hm_variates24_balanced(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24_zb(key ^ (base + (uint64_t)i), 32u);
 }
 uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
 }

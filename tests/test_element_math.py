@@ -34,6 +34,7 @@ def hm():
     L.hm_stream_key.restype = C.c_uint64
     L.hm_stream_key.argtypes = [C.c_uint64, C.c_uint64]
     L.hm_variates24.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_variates24_balanced.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     return L
 
 
@@ -70,6 +71,15 @@ def test_variate24_matches_reference_rng(hm, oracle):
         assert key == oracle.L.lpqo_stream_key(seed, call)
         for i in list(range(300)) + [2**40 + 3, 2**64 - 1]:
             assert hm.hm_variate24(key, i) * 2.0**-24 == oracle.variate(seed, call, i)
+
+
+def test_balanced_variate_form_is_identical(hm):
+    for key, base in [(0, 0), (0x5E41AB087439611E, 2**40), (2**64 - 1, 2**63)]:
+        a = np.empty(1 << 16, np.uint32)
+        b = np.empty(1 << 16, np.uint32)
+        hm.hm_variates24(key, base, a.size, a)
+        hm.hm_variates24_balanced(key, base, b.size, b)
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("fmt", FORMATS, ids=repr)
