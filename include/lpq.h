@@ -50,7 +50,9 @@ typedef enum {
   LPQ_ERR_ARGUMENT = 6,      /* null pointer, negative extent, bad mode     */
   LPQ_ERR_WORKSPACE = 7,     /* workspace too small                          */
   LPQ_ERR_CUDA = 8,          /* CUDA runtime error (lpq_last_cuda_error)     */
-  LPQ_ERR_NO_DEVICE = 9      /* no CUDA device / driver                      */
+  LPQ_ERR_NO_DEVICE = 9,     /* no CUDA device / driver                      */
+  LPQ_ERR_INVALID_VALUE = 10 /* invalid_value_error: non-finite result of a
+                                composed-chain op (tensor.cpp:58-78)         */
 } lpq_status;
 
 /* Rounding modes, in the order of proj/include/lpsim/formats.hpp:14-19. */
@@ -157,6 +159,19 @@ lpq_status lpq_uniform(float* y, int64_t n, uint64_t index_base, uint64_t seed,
 lpq_status lpq_variates(float* y, int64_t n, uint64_t index_base,
                         uint64_t seed, uint64_t call, void* stream);
 
+/* quantize_composed_at (proj/src/quant_ops.cpp:117-150, 166-177): the
+ * many-kernel baseline -- the same quantization as a chain of generic tensor
+ * kernels, one HBM pass and one temporary each (the paper's "many-kernel
+ * approach").  Float formats -> LPQ_ERR_UNSUPPORTED.
+ * ws: lpq_composed_workspace_size() bytes (three full-size temporaries). */
+size_t lpq_composed_workspace_size(const lpq_format* f, const int64_t* shape,
+                                   int rank);
+lpq_status lpq_quantize_composed(const float* x, float* y, const int64_t* shape,
+                                 int rank, uint64_t index_base,
+                                 const lpq_format* f, int mode, uint64_t seed,
+                                 uint64_t call, void* ws, size_t ws_bytes,
+                                 uint32_t* d_status, void* stream);
+
 /* ---- host entry points (synchronous; host buffers) ---------------------- */
 
 /* quantize_fused_at over host memory on CUDA device `device` (-1 = current):
@@ -165,6 +180,12 @@ lpq_status lpq_quantize_host(const float* x, float* y, const int64_t* shape,
                              int rank, uint64_t index_base,
                              const lpq_format* f, int mode, uint64_t seed,
                              uint64_t call, int device);
+
+lpq_status lpq_quantize_composed_host(const float* x, float* y,
+                                      const int64_t* shape, int rank,
+                                      uint64_t index_base, const lpq_format* f,
+                                      int mode, uint64_t seed, uint64_t call,
+                                      int device);
 
 lpq_status lpq_quant_gemm_host(const float* A, const float* B, float* C,
                                int64_t M, int64_t N, int64_t K,

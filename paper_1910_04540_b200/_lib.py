@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "liblpq.so")
 OK = 0
 ERR_FORMAT, ERR_SHAPE, ERR_INVALID_INPUT, ERR_UNSUPPORTED = 1, 2, 3, 4
 ERR_BLOCK_RANGE, ERR_ARGUMENT, ERR_WORKSPACE, ERR_CUDA, ERR_NO_DEVICE = 5, 6, 7, 8, 9
+ERR_INVALID_VALUE = 10
 
 
 class LpqFormat(C.Structure):
@@ -46,6 +47,10 @@ class UnsupportedFormatError(LpsimError):
     """unsupported_format_error."""
 
 
+class InvalidValueError(LpsimError):
+    """invalid_value_error: non-finite result of a composed-chain op."""
+
+
 class DeviceError(LpsimError):
     """CUDA runtime failure inside liblpq (no reference counterpart)."""
 
@@ -55,6 +60,7 @@ _EXC = {
     ERR_INVALID_INPUT: InvalidInputError, ERR_BLOCK_RANGE: InvalidInputError,
     ERR_UNSUPPORTED: UnsupportedFormatError, ERR_ARGUMENT: ValueError,
     ERR_WORKSPACE: ValueError, ERR_CUDA: DeviceError, ERR_NO_DEVICE: DeviceError,
+    ERR_INVALID_VALUE: InvalidValueError,
 }
 
 _F = C.POINTER(LpqFormat)
@@ -96,6 +102,13 @@ _PROTOS = {
     "lpq_matmul_q_host": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,
                                     C.c_int64, _F, C.c_int, C.c_uint64,
                                     C.c_uint64, C.c_int]),
+    "lpq_composed_workspace_size": (C.c_size_t, [_F, _I64P, C.c_int]),
+    "lpq_quantize_composed": (C.c_int, [_VP, _VP, _I64P, C.c_int, C.c_uint64,
+                                        _F, C.c_int, C.c_uint64, C.c_uint64,
+                                        _VP, C.c_size_t, _VP, _VP]),
+    "lpq_quantize_composed_host": (C.c_int, [_VP, _VP, _I64P, C.c_int,
+                                             C.c_uint64, _F, C.c_int,
+                                             C.c_uint64, C.c_uint64, C.c_int]),
     "lpq_shutdown": (None, []),
 }
 
@@ -116,7 +129,19 @@ def _load():
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """liblpq.so, loaded on first use (so the build recipe can import the
+    package before the library exists); a missing library raises loudly."""
+
+    _lib = None
+
+    def __getattr__(self, name):
+        if _LazyLib._lib is None:
+            _LazyLib._lib = _load()
+        return getattr(_LazyLib._lib, name)
+
+
+lib = _LazyLib()
 
 
 def status_string(st: int) -> str:

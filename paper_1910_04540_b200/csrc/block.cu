@@ -421,6 +421,36 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
 
 }  // namespace
 
+// Per-block max|x| (as uint bits) into maxima[extent] with the two-pass
+// plans' reduction kernels (used by the many-kernel baseline in composed.cu).
+cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
+                                uint32_t* maxima, cudaStream_t s) {
+  const int64_t n = g.outer * g.extent * g.stride;
+  cudaError_t e = cudaMemsetAsync(maxima, 0, sizeof(uint32_t) * g.extent, s);
+  if (e != cudaSuccess || n <= 0) return e;
+  if (g.stride >= 1024) {
+    const int64_t nseg = g.outer * g.extent;
+    const int64_t pieces = (g.stride + kPiece - 1) / kPiece;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)device_info().sm_count * 8, nseg * pieces));
+    if ((g.stride % 4 == 0) && aligned16(x))
+      k_seg_reduce<true><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+    else
+      k_seg_reduce<false><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+  } else {
+    const int64_t W = g.extent * g.stride;
+    const int64_t rpc = col_rows_per_chunk(g.outer, W);
+    dim3 grid((unsigned)((W + kColTile - 1) / kColTile),
+              (unsigned)((g.outer + rpc - 1) / rpc));
+    if ((W % 4 == 0) && aligned16(x))
+      k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+    else
+      k_col_reduce<false><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
   if (g.outer == 1 && g.stride % 4 == 0 && g.stride <= 32768 &&
       g.stride >= 64 && aligned16(x) && aligned16(y))

@@ -108,7 +108,10 @@ lpq_status block_geometry(const lpq_format* f, const int64_t* shape, int rank,
 }
 
 lpq_status map_status_bits(uint32_t bits) {
-  if (bits & kStatusBlockRange) return LPQ_ERR_BLOCK_RANGE;  // pass 1 throws first
+  // the earliest op of the reference's chain throws first: the composed
+  // chain's validation, then fused_block's pass 1, then the quantize pass
+  if (bits & kStatusInvalidValue) return LPQ_ERR_INVALID_VALUE;
+  if (bits & kStatusBlockRange) return LPQ_ERR_BLOCK_RANGE;
   if (bits & kStatusNonFinite) return LPQ_ERR_INVALID_INPUT;
   return LPQ_OK;
 }
@@ -173,6 +176,7 @@ const char* lpq_status_string(lpq_status s) {
     case LPQ_ERR_WORKSPACE: return "workspace too small";
     case LPQ_ERR_CUDA: return "CUDA runtime error";
     case LPQ_ERR_NO_DEVICE: return "no CUDA device available";
+    case LPQ_ERR_INVALID_VALUE: return "invalid_value_error: non-finite result";
   }
   return "unknown status";
 }

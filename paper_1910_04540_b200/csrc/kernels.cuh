@@ -10,7 +10,8 @@
 namespace lpq {
 
 // Error bits the kernels OR into the caller's device status word.
-enum : uint32_t { kStatusNonFinite = 1u, kStatusBlockRange = 2u };
+enum : uint32_t { kStatusNonFinite = 1u, kStatusBlockRange = 2u,
+                  kStatusInvalidValue = 4u };
 
 struct DeviceInfo {
   int sm_count;
@@ -50,6 +51,9 @@ size_t block_workspace(const BlockGeom& g, BlockPlan p);
 cudaError_t launch_block(const float* x, float* y, const BlockGeom& g,
                          BlockPlan plan, uint64_t base, uint64_t key, int wl,
                          int mode, void* ws, uint32_t* status, cudaStream_t s);
+
+cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
+                                uint32_t* maxima, cudaStream_t s);
 
 // ---- generators -------------------------------------------------------------
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,

@@ -271,6 +271,29 @@ LPQ_HD FixedParams make_fixed(int wl, int fl, bool symmetric, bool saturate) {
 }
 
 // TINY: fl <= -1, where x * 2^fl can flush to zero (make_fixed: p.tiny).
+// Two's-complement fold of an integer-valued k = (kneg ? -1 : 1) * kmag into
+// the wl-bit code range (FixedFolder::fold, scalar_quant.hpp:50-62, exact
+// fmod semantics incl. the sign of a zero remainder, which follows k),
+// scaled by `down`.  kmag >= 2^24 is an integer m * 2^t with t >= 1 (inf:
+// t >= 105 > wl).
+LPQ_HD float fold_wrap(float kmag, bool kneg, const FixedParams& p, float down) {
+  uint32_t km;
+  if (kmag < 16777216.0f) {
+    km = (uint32_t)kmag;
+  } else {
+    const uint32_t ab = f2u(kmag);
+    const int t = (int)(ab >> 23) - 150;
+    const uint32_t m = (ab & 0x7FFFFFu) | 0x800000u;
+    km = (t >= 32) ? 0u : (m << t);
+  }
+  const uint32_t ks = kneg ? (0u - km) : km;
+  int32_t m = (int32_t)(ks & p.mask);
+  if (m >= p.half) m -= (int32_t)(p.mask + 1u);
+  if (m < p.kmin_i) m = p.kmin_i;
+  if (m == 0) return kneg ? -0.0f : 0.0f;
+  return fmul((float)m, down);
+}
+
 template <int M, bool SAT, bool TINY = true>
 LPQ_HD float quant_fixed(float x, const FixedParams& p, uint32_t v) {
   const float r = fmul(x, p.up);
@@ -284,24 +307,7 @@ LPQ_HD float quant_fixed(float x, const FixedParams& p, uint32_t v) {
     k = fminf(fmaxf(k, p.kmin), p.kmax);  // +-inf clamp too
     return fmul(k, p.down);
   }
-  // wrap: two's-complement fold of k (exact fmod semantics, incl. the sign
-  // of a zero remainder, which follows k)
-  uint32_t km;
-  if (kmag < 16777216.0f) {
-    km = (uint32_t)kmag;
-  } else {
-    // |k| = a is an integer m * 2^t, t >= 1 (or inf: t >= 104 > wl)
-    const uint32_t ab = f2u(a);
-    const int t = (int)(ab >> 23) - 150;
-    const uint32_t m = (ab & 0x7FFFFFu) | 0x800000u;
-    km = (t >= 32) ? 0u : (m << t);
-  }
-  const uint32_t ks = kneg ? (0u - km) : km;
-  int32_t m = (int32_t)(ks & p.mask);
-  if (m >= p.half) m -= (int32_t)(p.mask + 1u);
-  if (m < p.kmin_i) m = p.kmin_i;
-  if (m == 0) return kneg ? -0.0f : 0.0f;
-  return fmul((float)m, p.down);
+  return fold_wrap(kmag, kneg, p, p.down);
 }
 
 LPQ_HD float fma_rn(float a, float b, float c) {

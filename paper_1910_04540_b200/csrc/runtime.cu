@@ -333,6 +333,47 @@ lpq_status host_context_quantize(const float* x, float* y,
                            call);
 }
 
+lpq_status host_context_composed(const float* x, float* y,
+                                 const int64_t* shape, int rank,
+                                 uint64_t index_base, const lpq_format* f,
+                                 int mode, uint64_t seed, uint64_t call,
+                                 int device) {
+  lpq_status st = check_format(f);
+  if (st != LPQ_OK) return st;
+  if (f->kind == LPQ_FLOAT) return LPQ_ERR_UNSUPPORTED;
+  int64_t n = 0;
+  st = check_shape(shape, rank, &n);
+  if (st != LPQ_OK) return st;
+  if (f->kind == LPQ_BLOCK) {
+    BlockGeom g;
+    st = block_geometry(f, shape, rank, &g);
+    if (st != LPQ_OK) return st;
+  }
+  if (n == 0) return LPQ_OK;
+  if (!x || !y) return LPQ_ERR_ARGUMENT;
+  const int dev = resolve_device(device, &st);
+  if (dev < 0) return st;
+  DeviceGuard guard(dev);
+  HostCtx* c = context_for(dev);
+  std::lock_guard<std::mutex> lk(c->mu);
+  LPQ_TRY(c->init());
+  LPQ_TRY(c->ensure_full(n));
+  const size_t wsb = lpq_composed_workspace_size(f, shape, rank);
+  LPQ_TRY(c->ensure_ws(wsb));
+  cudaStream_t s = c->st[0];
+  const size_t bytes = sizeof(float) * (size_t)n;
+  LPQ_TRY(cudaMemcpyAsync(c->dfull, x, bytes, cudaMemcpyHostToDevice, s));
+  st = quantize_composed_device(c->dfull, c->dfull, shape, rank, index_base, f,
+                                mode, seed, call, c->ws, c->ws_bytes,
+                                c->d_status, s);
+  if (st != LPQ_OK) {
+    cudaStreamSynchronize(s);
+    return st;
+  }
+  LPQ_TRY(cudaMemcpyAsync(y, c->dfull, bytes, cudaMemcpyDeviceToHost, s));
+  return lpq_status_fetch(c->d_status, s);
+}
+
 void shutdown_contexts() {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   g_ctx.clear();
@@ -347,6 +388,15 @@ lpq_status lpq_quantize_host(const float* x, float* y, const int64_t* shape,
                              const lpq_format* f, int mode, uint64_t seed,
                              uint64_t call, int device) {
   return lpq::host_context_quantize(x, y, shape, rank, index_base, f, mode,
+                                    seed, call, device);
+}
+
+lpq_status lpq_quantize_composed_host(const float* x, float* y,
+                                      const int64_t* shape, int rank,
+                                      uint64_t index_base, const lpq_format* f,
+                                      int mode, uint64_t seed, uint64_t call,
+                                      int device) {
+  return lpq::host_context_composed(x, y, shape, rank, index_base, f, mode,
                                     seed, call, device);
 }
 

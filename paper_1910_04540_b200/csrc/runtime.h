@@ -22,6 +22,13 @@ lpq_status quantize_device(const float* x, float* y, const int64_t* shape,
                            size_t ws_bytes, uint32_t* d_status,
                            cudaStream_t s);
 
+lpq_status quantize_composed_device(const float* x, float* y,
+                                    const int64_t* shape, int rank,
+                                    uint64_t index_base, const lpq_format* f,
+                                    int mode, uint64_t seed, uint64_t call,
+                                    void* ws, size_t ws_bytes,
+                                    uint32_t* status, cudaStream_t s);
+
 // Scoped cudaSetDevice (restores the caller's device).
 class DeviceGuard {
  public:

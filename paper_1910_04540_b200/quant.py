@@ -26,8 +26,9 @@ from typing import Optional, Union
 import numpy as np
 
 from . import _lib
-from ._lib import (FormatError, InvalidInputError, LpqFormat, ShapeError,
-                   UnsupportedFormatError, check, lib, shape_array)
+from ._lib import (FormatError, InvalidInputError, InvalidValueError,
+                   LpqFormat, ShapeError, UnsupportedFormatError, check, lib,
+                   shape_array)
 
 try:  # torch is plumbing for device memory and streams, not a dependency of the math
     import torch
@@ -232,6 +233,47 @@ def quantize_fused(t, spec: QuantSpec, **kw):
     return out
 
 
+def quantize_composed_at(t, spec: QuantSpec, call: int, *, index_base: int = 0,
+                         sync: bool = True):
+    """quantize_composed_at (quant_ops.cpp:166-177): the many-kernel baseline
+    (one kernel and HBM pass per tensor op).  Float formats raise
+    UnsupportedFormatError."""
+    fmt = spec.format.c()
+    if _is_device(t):
+        x = t.contiguous()
+        y = torch.empty_like(x)
+        shape = shape_array(x.shape)
+        nbytes = lib.lpq_composed_workspace_size(C.byref(fmt), shape, x.dim())
+        ws = _workspace(x.device, nbytes)
+        with torch.cuda.device(x.device):
+            st = lib.lpq_quantize_composed(
+                C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), shape,
+                x.dim(), int(index_base), C.byref(fmt), int(spec.mode),
+                int(spec.seed), int(call),
+                C.c_void_p(ws.data_ptr() if ws is not None else 0), nbytes,
+                C.c_void_p(_status_buf(x.device).data_ptr()), _stream_ptr(x.device))
+            check(st, "quantize_composed")
+            if sync:
+                fetch_status(x.device)
+        return y
+    is_torch = torch is not None and isinstance(t, torch.Tensor)
+    x = t.detach().contiguous().numpy() if is_torch else np.ascontiguousarray(t)
+    y = np.empty_like(x)
+    st = lib.lpq_quantize_composed_host(
+        C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data),
+        shape_array(x.shape), x.ndim, int(index_base), C.byref(fmt),
+        int(spec.mode), int(spec.seed), int(call), -1)
+    check(st, "quantize_composed")
+    return torch.from_numpy(y) if is_torch else y
+
+
+def quantize_composed(t, spec: QuantSpec, **kw):
+    out = quantize_composed_at(t, spec, spec.call_counter, **kw)
+    if spec.mode == RoundingMode.Stochastic:
+        spec.call_counter += 1
+    return out
+
+
 def quantized_op(op, spec: QuantSpec):
     """quantized_op (quant_ops.hpp:36-42): quantize_fused appended to op."""
     def run(*args, **kwargs):
@@ -367,8 +409,10 @@ def variate_tensor(shape, seed: int, call: int, *, device="cuda",
 __all__ = [
     "RoundingMode", "FloatFormat", "FixedFormat", "BlockFloatFormat",
     "NumberFormat", "QuantSpec", "validate", "quantize_fused",
-    "quantize_fused_at", "quantized_op", "quantized_matmul",
+    "quantize_fused_at", "quantize_composed", "quantize_composed_at",
+    "quantized_op", "quantized_matmul",
     "quantized_matmul_at", "quant_gemm", "random_uniform", "variate_tensor",
     "pass_count", "reset_pass_count", "launch_count", "fetch_status",
-    "InvalidInputError", "ShapeError", "FormatError", "UnsupportedFormatError",
+    "InvalidInputError", "InvalidValueError", "ShapeError", "FormatError",
+    "UnsupportedFormatError",
 ]
