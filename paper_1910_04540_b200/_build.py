@@ -100,6 +100,52 @@ def build_host_math(force=False, verbose=False):
     return HOST_MATH
 
 
+REF = "/root/reference/proj"
+JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+DROPIN = os.path.join(ROOT, "build", "dropin")
+
+
+def build_dropin(force=False, verbose=False):
+    """TEST ONLY: the reference library with proj/src/quant_ops.cpp replaced
+    by the B200 drop-in (csrc/dropin/quant_ops_b200.cpp over liblpq.so), and
+    the reference's own unit suites (compiled unchanged against a minimal
+    doctest header) and acceptance binary linked against it.  Needs the
+    reference sources, so it is built here and the binaries travel."""
+    if not os.path.isdir(REF):
+        return None
+    os.makedirs(DROPIN, exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    inc = ["-I", os.path.join(REF, "include"), "-I", os.path.join(ROOT, "include"),
+           "-I", JSON_INC]
+    flags = ["-std=c++20", "-O2", "-fPIC", "-w"]
+    shim = os.path.join(CSRC, "dropin", "quant_ops_b200.cpp")
+    srcs = [os.path.join(REF, "src", f) for f in
+            ("tensor.cpp", "enumerate.cpp", "train.cpp", "bench.cpp", "io.cpp")] + [shim]
+    objs, jobs = [], []
+    for src in srcs:
+        o = os.path.join(DROPIN, os.path.basename(src).replace(".cpp", ".o"))
+        objs.append(o)
+        if force or _newer(o, [src, os.path.join(ROOT, "include", "lpq.h")]):
+            jobs.append([cxx, *flags, *inc, "-c", src, "-o", o])
+    with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
+        list(ex.map(lambda c: _run(c, verbose), jobs))
+    link = ["-L", LIBDIR, "-llpq", f"-Wl,-rpath,{LIBDIR}",
+            "-Wl,-rpath,$ORIGIN/../../paper_1910_04540_b200/lib", "-lpthread"]
+    main = os.path.join(ROOT, "tests", "native", "doctest_main.cpp")
+    tests = [os.path.join(REF, "tests", f) for f in
+             ("test_quant_ops.cpp", "test_train.cpp", "test_bench.cpp")]
+    tinc = ["-I", os.path.join(ROOT, "tests", "native", "doctest_mini"),
+            "-I", os.path.join(REF, "tests")]
+    out_t = os.path.join(DROPIN, "lpsim_tests_b200")
+    if force or jobs or _newer(out_t, [main, LIB] + tests + objs):
+        _run([cxx, *flags, *inc, *tinc, main, *tests, *objs, "-o", out_t, *link], verbose)
+    out_a = os.path.join(DROPIN, "lpsim_acceptance_b200")
+    acc = os.path.join(REF, "tests", "acceptance.cpp")
+    if force or jobs or _newer(out_a, [acc, LIB] + objs):
+        _run([cxx, *flags, *inc, *tinc, acc, *objs, "-o", out_a, *link], verbose)
+    return out_t, out_a
+
+
 def build_oracle(verbose=False):
     _run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], verbose)
 
@@ -107,7 +153,9 @@ def build_oracle(verbose=False):
 def build_all(force=False, verbose=False):
     build_oracle(verbose)
     build_host_math(force, verbose)
-    return build_lib(force, verbose)
+    lib = build_lib(force, verbose)
+    build_dropin(force, verbose)
+    return lib
 
 
 if __name__ == "__main__":
