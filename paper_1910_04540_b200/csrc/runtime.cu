@@ -200,8 +200,12 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
                            int64_t unit, bool rows, uint64_t index_base,
                            const lpq_format* f, int mode, uint64_t seed,
                            uint64_t call) {
-  const int64_t chunk = std::max<int64_t>(1, kChunkElems / unit) * unit;
-  LPQ_TRY(c->ensure_chunks(chunk));
+  // at least ~4 chunks when the tensor allows, so even mid-size tensors
+  // overlap copy-in, kernel and copy-out; 64 MiB chunks at most
+  const int64_t target = std::min<int64_t>(
+      kChunkElems, std::max<int64_t>(int64_t(1) << 18, (n + 3) / 4));
+  const int64_t chunk = std::max<int64_t>(1, target / unit) * unit;
+  LPQ_TRY(c->ensure_chunks(std::max<int64_t>(chunk, c->chunk_cap)));
   const bool pin_x = is_pinned(x), pin_y = is_pinned(y);
   const int64_t nchunks = (n + chunk - 1) / chunk;
   lpq_format fr = *f;
