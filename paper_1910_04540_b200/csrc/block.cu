@@ -139,11 +139,8 @@ template <int M, int T, int VPT>
 void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
                    uint64_t base, uint64_t key, int wl, uint32_t* st,
                    cudaStream_t s) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                k_block_rows<M, T, VPT>, T, 0);
-  const int64_t cap = (int64_t)device_info().sm_count * std::max(per_sm, 1);
-  const int grid = (int)std::max<int64_t>(1, std::min(cap, nrows));
+  // one CTA per row, all rows launched (CTAs retire in address order)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, 0x7FFFFFFF));
   k_block_rows<M, T, VPT><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, st);
   note_launch();
 }

@@ -21,7 +21,7 @@ namespace lpq {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;  // 8 float4 = 128 B in flight per thread
 
 template <bool TINY>
 struct FixedSatOp {
@@ -140,19 +140,14 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   const int64_t head = vector_head(x, y, n);
   const int64_t n4 = (n - head) >> 2;
   const int64_t work = std::max<int64_t>(n4, n - 4 * n4);
-  const DeviceInfo& di = device_info();
   const bool idx4 = ((base + (uint64_t)head) & 3u) == 0;
-  int per_sm = 0;
-  if (idx4)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_elementwise<M, Op, true>, kThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_elementwise<M, Op, false>, kThreads, 0);
-  const int64_t cap = (int64_t)di.sm_count * std::max(per_sm, 1);
+  // One trip per thread over the whole tensor (not a persistent grid): CTAs
+  // retire and launch in address order, which keeps the DRAM pages in use
+  // compact.  Measured on B200 (scripts/ew_variants.cu, 2^30 elements):
+  // persistent grid-stride 5.85 TB/s vs one-trip 8 x float4 6.59 TB/s.
   const int64_t want = (work + (int64_t)kThreads * kUnroll - 1) /
                        ((int64_t)kThreads * kUnroll);
-  const int grid = (int)std::max<int64_t>(1, std::min(cap, want));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
   if (idx4)
     k_elementwise<M, Op, true><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
                                                          key, op, 32u, status);

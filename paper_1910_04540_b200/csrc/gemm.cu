@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kQT)
     const int buf = (int)(kt & 1);
     if (kt + 1 < nk) load((kt + 1) * kBK);
     const int kk_end = (int)min((int64_t)kBK, K - kt * kBK);
-    for (int kk = 0; kk < kk_end; ++kk) {
+    auto step = [&](int kk) {
       const uint4 av = *reinterpret_cast<const uint4*>(&As[buf][kk][ty * 8]);
       const uint4 b0 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16]);
       const uint4 b1 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16 + 8]);
@@ -214,6 +214,14 @@ __global__ void __launch_bounds__(kQT)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = badd2(acc[i][j], bmul2(a2, bw[j]));
       }
+    };
+    if (kk_end == kBK) {
+      // full tile: unrolled so the shared-memory loads of k+1 overlap the
+      // math of k (the k order of every accumulator is unchanged)
+#pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kk_end; ++kk) step(kk);
     }
     if (kt + 1 < nk) stash(buf ^ 1);
     __syncthreads();
