@@ -181,6 +181,8 @@ CONFIGS = {
     "c1n": dict(workload="C1: float exp=5 man=2, nearest-even, 2^24 elements per GPU "
                          "(rotating buffers > L2)",
                 kind="float", n=1 << 24, fmt=("float", 5, 2), mode="nearest_even"),
+    "c1big": dict(workload="float exp=5 man=2, stochastic, 2^30 elements (diagnostic)",
+                  kind="float", n=1 << 30, fmt=("float", 5, 2), mode="stochastic"),
     "c2": dict(workload="C2: fixed-point wl=8 fl=4 saturating, stochastic rounding, "
                         "2^30-element fp32 tensor per GPU",
                kind="fixed", n=1 << 30, fmt=("fixed", 8, 4), mode="stochastic"),
@@ -435,6 +437,119 @@ def run_gemm(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
+def run_sweep(args, rank, world, local_rank):
+    """C5: ResNet-50 training-step quantization sweep (batch 256): the 54
+    weight, 54 weight-gradient and 54 activation tensors, each through
+    float(5,2), fixed(8,4) and block(8, dim 0) (per output channel for
+    weights and gradients, per sample for activations); nearest-even for
+    weights and activations, stochastic for gradients.  One step = the whole
+    sweep (486 quantizations), captured once as a CUDA graph and replayed."""
+    import torch
+    import torch.distributed as dist
+    import ctypes as C
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200 import _lib
+    from paper_1910_04540_b200.resnet50 import numel, resnet50_layers
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    layers = resnet50_layers(256)
+    fmts = [q.FloatFormat(5, 2), q.FixedFormat(8, 4), q.BlockFloatFormat(8, 0)]
+    tensors = []  # (tensor, mode)
+    for i, (name, wshape, ashape) in enumerate(layers):
+        tensors.append((q.random_uniform(wshape, 100 + i, 0, -0.1, 0.1, device=dev),
+                        q.RoundingMode.NearestEven))
+        tensors.append((q.random_uniform(wshape, 200 + i, 0, -1e-3, 1e-3, device=dev),
+                        q.RoundingMode.Stochastic))
+        tensors.append((q.random_uniform(ashape, 300 + i, 0, -4.0, 4.0, device=dev),
+                        q.RoundingMode.NearestEven))
+    out = torch.empty(max(t.numel() for t, _ in tensors), device=dev)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+    status = q.quant._status_buf(dev)
+    calls = []
+    for t, mode in tensors:
+        shp = _lib.shape_array(t.shape)
+        for f in fmts:
+            calls.append((C.c_void_p(t.data_ptr()), C.c_void_p(out.data_ptr()), shp,
+                          t.dim(), f.c(), int(mode), t.numel()))
+
+    def sweep(stream):
+        sp = C.c_void_p(stream.cuda_stream)
+        for xp, yp, shp, rank_, fc, mode, n in calls:
+            _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode,
+                                             SEED, 0, C.c_void_p(ws.data_ptr()),
+                                             ws.numel(), C.c_void_p(status.data_ptr()),
+                                             sp), "sweep")
+
+    # algorithmic bytes from the passes the library makes (8 B/elem single
+    # pass, 12 B/elem two-pass block plans)
+    q.reset_pass_count()
+    l0 = q.launch_count()
+    nbytes = 0
+    s0 = torch.cuda.current_stream(dev)
+    for xp, yp, shp, rank_, fc, mode, n in calls:
+        p0 = q.pass_count()
+        _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode, SEED, 0,
+                                         C.c_void_p(ws.data_ptr()), ws.numel(),
+                                         C.c_void_p(status.data_ptr()),
+                                         C.c_void_p(s0.cuda_stream)))
+        nbytes += (8 if q.pass_count() - p0 == 1 else 12) * n
+    launches_per_sweep = q.launch_count() - l0
+    q.fetch_status(dev)
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(s0)
+    with torch.cuda.stream(side):
+        sweep(side)  # warm the side stream
+    s0.wait_stream(side)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=side):
+        sweep(side)
+    for _ in range(args.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    q.fetch_status(dev)
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        t0.record(s0)
+        for _ in range(args.steps):
+            g.replay()
+        t1.record(s0)
+        torch.cuda.synchronize()
+    q.fetch_status(dev)
+    el = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    peak, peak_src, _ = load_peaks()
+    ach = nbytes * args.steps / el / 1e9
+    total_elems = sum(t.numel() for t, _ in tensors)
+    return {
+        "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
+        "value": round(ach * world, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (u32/fp32 bit arithmetic)",
+        "data": "synthetic ResNet-50-shaped tensors (no weights available offline)",
+        "config": {"workload": "C5: ResNet-50 (batch 256) weights, weight gradients and "
+                               "activations through float(5,2), fixed(8,4), block(8, dim0)",
+                   "tensors": len(tensors), "quantizations_per_step": len(calls),
+                   "elements_per_sweep_pass": total_elems,
+                   "algorithmic_bytes_per_step": nbytes,
+                   "launches_per_step": launches_per_sweep,
+                   "parallelism": f"replica{world}"},
+        "gpu_launches": launches_per_sweep * args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+    }
+
+
+# ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU quantize_fused_at on the host."""
     if rank != 0:
@@ -487,7 +602,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
@@ -499,7 +614,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        if args.config == "c4":
+        if args.config in ("c4", "c5"):
             args.config = "c2"
         out = run_reference(args, rank, world)
         if out is not None:
@@ -510,7 +625,8 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = (run_gemm if args.config == "c4" else run_ours)(args, rank, world, local_rank)
+    runner = {"c4": run_gemm, "c5": run_sweep}.get(args.config, run_ours)
+    out = runner(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -42,27 +42,40 @@ __device__ __forceinline__ uint32_t nf4(const float4& v) {
 
 // TWO: the block's scales need two factors (maxima near the fp32 range
 // ends); uniform per block, so kernels branch once per block/row.
+// z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
 template <int M, bool TWO>
 __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
-                                    float kmax, uint64_t key, uint64_t idx) {
+                                    float kmax, uint64_t z, uint32_t m32) {
   uint32_t v = 0;
-  if (M == kStochastic) v = variate24(key, idx);
+  if (M == kStochastic) v = variate24_zb(z, m32);
   if (M == kNearestEven || M == kStochastic)
     return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
         x, s, kmin, kmax, v);
   return quant_block<M>(x, s, kmin, kmax, v);
 }
 
-template <int M, bool TWO>
+// IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q
+template <int M, bool TWO, bool IDX4>
 __device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
                                       float kmin, float kmax, uint64_t key,
-                                      uint64_t idx) {
+                                      uint64_t idx, uint32_t m32) {
+  const uint64_t z0 = key ^ idx;
   float4 o;
-  o.x = qb<M, TWO>(x.x, s, kmin, kmax, key, idx);
-  o.y = qb<M, TWO>(x.y, s, kmin, kmax, key, idx + 1);
-  o.z = qb<M, TWO>(x.z, s, kmin, kmax, key, idx + 2);
-  o.w = qb<M, TWO>(x.w, s, kmin, kmax, key, idx + 3);
+  o.x = qb<M, TWO>(x.x, s, kmin, kmax, z0, m32);
+  o.y = qb<M, TWO>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
+  o.z = qb<M, TWO>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);
+  o.w = qb<M, TWO>(x.w, s, kmin, kmax, IDX4 ? z0 ^ 3u : key ^ (idx + 3), m32);
   return o;
+}
+
+// |x| maximum with NaN ignored (fmaxf returns the non-NaN operand, like
+// `a > m` in reduce_max_abs); nf = x * 0 + nf turns NaN on any non-finite x.
+__device__ __forceinline__ void absmax_nf(const float4& v, float& m, float& nf) {
+  m = fmaxf(fmaxf(m, fabsf(v.x)), fmaxf(fabsf(v.y), fmaxf(fabsf(v.z), fabsf(v.w))));
+  nf = __fmaf_rn(v.x, 0.0f, nf);
+  nf = __fmaf_rn(v.y, 0.0f, nf);
+  nf = __fmaf_rn(v.z, 0.0f, nf);
+  nf = __fmaf_rn(v.w, 0.0f, nf);
 }
 
 __device__ __forceinline__ bool two_factor(const BlockScale& s) {
@@ -76,11 +89,11 @@ __device__ __forceinline__ void flag(uint32_t* status, uint32_t bits) {
 // ---------------------------------------------------------------------------
 // Plan 1: one row per CTA, held in registers (single HBM pass).
 // T threads, VPT float4 per thread; row length L (multiple of 4, <= 4*T*VPT).
-template <int M, int T, int VPT>
+template <int M, int T, int VPT, bool IDX4>
 __global__ void __launch_bounds__(T)
     k_block_rows(const float* __restrict__ x, float* __restrict__ y, int64_t L,
                  int64_t nrows, uint64_t base, uint64_t key, int wl,
-                 uint32_t* __restrict__ status) {
+                 uint32_t m32, uint32_t* __restrict__ status) {
   __shared__ uint32_t red[T / 32];
   __shared__ uint32_t row_max;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -88,21 +101,21 @@ __global__ void __launch_bounds__(T)
   const float kmax = (float)((1 << (wl - 1)) - 1);
   const int64_t L4 = L >> 2;
   uint32_t bad = 0;
+  float nf = 0.0f;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
     float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
     float4 v[VPT];
-    uint32_t m = 0;
+    float mf = 0.0f;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int64_t j = threadIdx.x + (int64_t)k * T;
       if (j < L4) {
         v[k] = __ldcs(xr + j);
-        m = max(m, max4(v[k]));
-        bad |= nf4(v[k]);
+        absmax_nf(v[k], mf, nf);
       }
     }
-    m = __reduce_max_sync(kFull, m);
+    uint32_t m = __reduce_max_sync(kFull, f2u(mf));  // non-negative: uint order
     if (lane == 0) red[warp] = m;
     __syncthreads();
     if (warp == 0) {
@@ -119,18 +132,21 @@ __global__ void __launch_bounds__(T)
       for (int k = 0; k < VPT; ++k) {
         const int64_t j = threadIdx.x + (int64_t)k * T;
         if (j < L4)
-          __stcs(yr + j, qb4<M, false>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+          __stcs(yr + j, qb4<M, false, IDX4>(v[k], sc, kmin, kmax, key,
+                                             row_base + 4 * j, m32));
       }
     } else {
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
         const int64_t j = threadIdx.x + (int64_t)k * T;
         if (j < L4)
-          __stcs(yr + j, qb4<M, true>(v[k], sc, kmin, kmax, key, row_base + 4 * j));
+          __stcs(yr + j, qb4<M, true, IDX4>(v[k], sc, kmin, kmax, key,
+                                            row_base + 4 * j, m32));
       }
     }
     __syncthreads();  // red/row_max are reused by the next row
   }
+  if (nf != nf) bad |= 1u;
   bad = __reduce_or_sync(kFull, bad);
   if (lane == 0) flag(status, bad);
 }
@@ -141,7 +157,10 @@ void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
                    cudaStream_t s) {
   // one CTA per row, all rows launched (CTAs retire in address order)
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, 0x7FFFFFFF));
-  k_block_rows<M, T, VPT><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, st);
+  if ((base & 3u) == 0)
+    k_block_rows<M, T, VPT, true><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, 32u, st);
+  else
+    k_block_rows<M, T, VPT, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, 32u, st);
   note_launch();
 }
 
@@ -238,15 +257,15 @@ __global__ void __launch_bounds__(kSegT)
         if (4 * j < len) {
           bad |= nf4(v[k]);
           const uint64_t idx = base + (uint64_t)(e0 + 4 * j);
-          __stcs(y4 + j, two ? qb4<M, true>(v[k], sc, kmin, kmax, key, idx)
-                             : qb4<M, false>(v[k], sc, kmin, kmax, key, idx));
+          __stcs(y4 + j, two ? qb4<M, true, false>(v[k], sc, kmin, kmax, key, idx, 32u)
+                             : qb4<M, false, false>(v[k], sc, kmin, kmax, key, idx, 32u));
         }
       }
     } else {
       for (int j = threadIdx.x; j < len; j += kSegT) {
         const float xv = x[e0 + j];
         bad |= nonfinite(xv) ? 1u : 0u;
-        y[e0 + j] = qb<M, true>(xv, sc, kmin, kmax, key, base + (uint64_t)(e0 + j));
+        y[e0 + j] = qb<M, true>(xv, sc, kmin, kmax, key ^ (base + (uint64_t)(e0 + j)), 32u);
       }
     }
   }
@@ -331,10 +350,10 @@ __global__ void __launch_bounds__(kColT)
       const float4 v = load4<VEC>(x + r * W, c, W);
       const uint64_t idx = base + (uint64_t)(r * W + c);
       float4 o;
-      o.x = qb<M, true>(v.x, s[0], kmin, kmax, key, idx);
-      o.y = qb<M, true>(v.y, s[1], kmin, kmax, key, idx + 1);
-      o.z = qb<M, true>(v.z, s[2], kmin, kmax, key, idx + 2);
-      o.w = qb<M, true>(v.w, s[3], kmin, kmax, key, idx + 3);
+      o.x = qb<M, true>(v.x, s[0], kmin, kmax, key ^ idx, 32u);
+      o.y = qb<M, true>(v.y, s[1], kmin, kmax, key ^ (idx + 1), 32u);
+      o.z = qb<M, true>(v.z, s[2], kmin, kmax, key ^ (idx + 2), 32u);
+      o.w = qb<M, true>(v.w, s[3], kmin, kmax, key ^ (idx + 3), 32u);
       if (VEC) {
         bad |= nf4(v);
         __stcs(reinterpret_cast<float4*>(y + r * W + c), o);
