@@ -45,9 +45,9 @@ __device__ __forceinline__ uint32_t nf4(const float4& v) {
 // z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
 template <int M, bool TWO>
 __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
-                                    float kmax, uint64_t z, uint32_t m32) {
+                                    float kmax, uint64_t z, const RngMul& rm) {
   uint32_t v = 0;
-  if (M == kStochastic) v = variate24_zb(z, m32);
+  if (M == kStochastic) v = variate24_zb(z, rm.m32);
   if (M == kNearestEven || M == kStochastic)
     return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
         x, s, kmin, kmax, v);
@@ -58,7 +58,7 @@ __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
 template <int M, bool TWO, bool IDX4>
 __device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
                                       float kmin, float kmax, uint64_t key,
-                                      uint64_t idx, uint32_t m32) {
+                                      uint64_t idx, const RngMul& m32) {
   const uint64_t z0 = key ^ idx;
   float4 o;
   o.x = qb<M, TWO>(x.x, s, kmin, kmax, z0, m32);
@@ -93,7 +93,7 @@ template <int M, int T, int VPT, bool IDX4>
 __global__ void __launch_bounds__(T)
     k_block_rows(const float* __restrict__ x, float* __restrict__ y, int64_t L,
                  int64_t nrows, uint64_t base, uint64_t key, int wl,
-                 uint32_t m32, uint32_t* __restrict__ status) {
+                 RngMul m32, uint32_t* __restrict__ status) {
   __shared__ uint32_t red[T / 32];
   __shared__ uint32_t row_max;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -158,9 +158,9 @@ void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
   // one CTA per row, all rows launched (CTAs retire in address order)
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, 0x7FFFFFFF));
   if ((base & 3u) == 0)
-    k_block_rows<M, T, VPT, true><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, 32u, st);
+    k_block_rows<M, T, VPT, true><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   else
-    k_block_rows<M, T, VPT, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, 32u, st);
+    k_block_rows<M, T, VPT, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   note_launch();
 }
 
@@ -257,15 +257,15 @@ __global__ void __launch_bounds__(kSegT)
         if (4 * j < len) {
           bad |= nf4(v[k]);
           const uint64_t idx = base + (uint64_t)(e0 + 4 * j);
-          __stcs(y4 + j, two ? qb4<M, true, false>(v[k], sc, kmin, kmax, key, idx, 32u)
-                             : qb4<M, false, false>(v[k], sc, kmin, kmax, key, idx, 32u));
+          __stcs(y4 + j, two ? qb4<M, true, false>(v[k], sc, kmin, kmax, key, idx, rng_mul())
+                             : qb4<M, false, false>(v[k], sc, kmin, kmax, key, idx, rng_mul()));
         }
       }
     } else {
       for (int j = threadIdx.x; j < len; j += kSegT) {
         const float xv = x[e0 + j];
         bad |= nonfinite(xv) ? 1u : 0u;
-        y[e0 + j] = qb<M, true>(xv, sc, kmin, kmax, key ^ (base + (uint64_t)(e0 + j)), 32u);
+        y[e0 + j] = qb<M, true>(xv, sc, kmin, kmax, key ^ (base + (uint64_t)(e0 + j)), rng_mul());
       }
     }
   }
@@ -350,10 +350,10 @@ __global__ void __launch_bounds__(kColT)
       const float4 v = load4<VEC>(x + r * W, c, W);
       const uint64_t idx = base + (uint64_t)(r * W + c);
       float4 o;
-      o.x = qb<M, true>(v.x, s[0], kmin, kmax, key ^ idx, 32u);
-      o.y = qb<M, true>(v.y, s[1], kmin, kmax, key ^ (idx + 1), 32u);
-      o.z = qb<M, true>(v.z, s[2], kmin, kmax, key ^ (idx + 2), 32u);
-      o.w = qb<M, true>(v.w, s[3], kmin, kmax, key ^ (idx + 3), 32u);
+      o.x = qb<M, true>(v.x, s[0], kmin, kmax, key ^ idx, rng_mul());
+      o.y = qb<M, true>(v.y, s[1], kmin, kmax, key ^ (idx + 1), rng_mul());
+      o.z = qb<M, true>(v.z, s[2], kmin, kmax, key ^ (idx + 2), rng_mul());
+      o.w = qb<M, true>(v.w, s[3], kmin, kmax, key ^ (idx + 3), rng_mul());
       if (VEC) {
         bad |= nf4(v);
         __stcs(reinterpret_cast<float4*>(y + r * W + c), o);

@@ -25,6 +25,7 @@ constexpr int kUnroll = 8;  // 8 float4 = 128 B in flight per thread
 
 template <bool TINY>
 struct FixedSatOp {
+  static constexpr bool kFmaRng = false;  // FMA-pipe-bound already
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
@@ -33,20 +34,26 @@ struct FixedSatOp {
   }
 };
 struct FixedWrapOp {
+  static constexpr bool kFmaRng = true;
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
     return quant_fixed<M, false>(x, p, v);
   }
 };
-// FAST: the streaming form (even/stochastic, exp_bits >= 2)
-template <bool FAST>
+// V: 2 = scaled form (even/stochastic, 2 <= exp_bits <= 7), 1 = bit-surgery
+// streaming form (even/stochastic, exp_bits == 8), 0 = general
+template <int V>
 struct FloatOp {
+  static constexpr bool kFmaRng = V != 2;  // the scaled form is FMA-heavy
   FloatParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
-    if (FAST && (M == kNearestEven || M == kStochastic))
-      return quant_float_fast<M == kNearestEven ? kNearestEven : kStochastic>(x, p, v);
+    constexpr int MF = M == kNearestEven ? kNearestEven : kStochastic;
+    if (V == 2 && (M == kNearestEven || M == kStochastic))
+      return quant_float_scaled<MF>(x, p, v);
+    if (V == 1 && (M == kNearestEven || M == kStochastic))
+      return quant_float_fast<MF>(x, p, v);
     return quant_float<M>(x, p, v);
   }
 };
@@ -59,9 +66,10 @@ struct FloatOp {
 // turns NaN for any +-inf or NaN.
 template <int M, class Op>
 __device__ __forceinline__ float qelem(const Op& op, float x, uint64_t z,
-                                       uint32_t m32, float& nf) {
+                                       const RngMul& rm, float& nf) {
   uint32_t v = 0;
-  if (M == kStochastic) v = variate24_zb(z, m32);
+  if (M == kStochastic)
+    v = Op::kFmaRng ? variate24_zf(z, rm) : variate24_zb(z, rm.m32);
   nf = __fmaf_rn(x, 0.0f, nf);
   return op.template apply<M>(x, v);
 }
@@ -72,7 +80,7 @@ template <int M, class Op, bool IDX4>
 __global__ void __launch_bounds__(kThreads)
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
-                  uint32_t m32, uint32_t* __restrict__ status) {
+                  RngMul rm, uint32_t* __restrict__ status) {
   const int64_t n4 = (n - head) >> 2;
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
@@ -104,10 +112,10 @@ __global__ void __launch_bounds__(kThreads)
           z3 = key ^ (idx + 3);
         }
         float4 o;
-        o.x = qelem<M>(op, v[u].x, z0, m32, nf);
-        o.y = qelem<M>(op, v[u].y, z1, m32, nf);
-        o.z = qelem<M>(op, v[u].z, z2, m32, nf);
-        o.w = qelem<M>(op, v[u].w, z3, m32, nf);
+        o.x = qelem<M>(op, v[u].x, z0, rm, nf);
+        o.y = qelem<M>(op, v[u].y, z1, rm, nf);
+        o.z = qelem<M>(op, v[u].z, z2, rm, nf);
+        o.w = qelem<M>(op, v[u].w, z3, rm, nf);
         __stcs(y4 + j, o);
       }
     }
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < extra;
        t += (int64_t)gridDim.x * kThreads) {
     const int64_t e = t < head ? t : tail0 + (t - head);
-    y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), m32, nf);
+    y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), rm, nf);
   }
   if (__any_sync(0xFFFFFFFFu, nf != nf) && (threadIdx.x & 31) == 0)
     atomicOr(status, kStatusNonFinite);
@@ -150,10 +158,10 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
   if (idx4)
     k_elementwise<M, Op, true><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                         key, op, 32u, status);
+                                                         key, op, rng_mul(), status);
   else
     k_elementwise<M, Op, false><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                          key, op, 32u, status);
+                                                          key, op, rng_mul(), status);
   note_launch();
   return cudaGetLastError();
 }
@@ -211,9 +219,11 @@ cudaError_t launch_fixed(const float* x, float* y, int64_t n, uint64_t base,
 cudaError_t launch_float(const float* x, float* y, int64_t n, uint64_t base,
                          uint64_t key, const FloatParams& p, int mode,
                          uint32_t* status, cudaStream_t s) {
+  if (p.scaled_ok)
+    return dispatch_mode(x, y, n, base, key, FloatOp<2>{p}, mode, status, s);
   if (!p.tiny)
-    return dispatch_mode(x, y, n, base, key, FloatOp<true>{p}, mode, status, s);
-  return dispatch_mode(x, y, n, base, key, FloatOp<false>{p}, mode, status, s);
+    return dispatch_mode(x, y, n, base, key, FloatOp<1>{p}, mode, status, s);
+  return dispatch_mode(x, y, n, base, key, FloatOp<0>{p}, mode, status, s);
 }
 
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,

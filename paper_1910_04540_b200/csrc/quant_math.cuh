@@ -187,6 +187,50 @@ LPQ_HD uint32_t variate24_zb(uint64_t z, uint32_t m32) {
 
 LPQ_HD float variate_float(uint32_t v) { return (float)v * 0x1p-24f; }
 
+// Runtime multipliers for the FMA-pipe forms of shifts/adds (kernel
+// arguments, so ptxas cannot fold the multiplies back into SHF/IADD on the
+// ALU pipe).
+struct RngMul {
+  uint32_t one;   // 1
+  uint32_t m4;    // 4      (>> 30 as hi(x * 4))
+  uint32_t m32;   // 32     (>> 27 as hi(x * 32))
+  uint32_t m24;   // 2^24   (>> 8  as hi(x * 2^24))
+};
+
+LPQ_HD RngMul rng_mul() { return RngMul{1u, 4u, 32u, 1u << 24}; }
+
+LPQ_HD uint64_t mad_wide_u32(uint32_t a, uint32_t b, uint64_t c) {
+#if defined(__CUDA_ARCH__)
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+#else
+  return (uint64_t)a * b + c;
+#endif
+}
+
+// FMA-pipe-heavy form of variate24_z for the ALU-bound quantizers (float,
+// block): the 64-bit add, both xor-shifts and the final >> 8 run as
+// IMAD/IMAD.HI/IMAD.WIDE, leaving 5 ALU ops (xors) per variate.
+LPQ_HD uint32_t variate24_zf(uint64_t z, const RngMul& m) {
+  // z += C0: (lo * 1 + C0) as a 64-bit IMAD.WIDE, then the high word
+  const uint64_t t = mad_wide_u32((uint32_t)z, m.one, 0x9E3779B97F4A7C15ull);
+  uint32_t lo = (uint32_t)t;
+  uint32_t hi = (uint32_t)(z >> 32) * m.one + (uint32_t)(t >> 32);
+  // z ^= z >> 30
+  lo ^= umulhi32(lo, m.m4) + hi * m.m4;
+  hi ^= umulhi32(hi, m.m4);
+  // z *= C1
+  const uint64_t w = mad_wide_u32(lo, 0x1CE4E5B9u, 0ull);
+  hi = (uint32_t)(w >> 32) + lo * 0xBF58476Du + hi * 0x1CE4E5B9u;
+  lo = (uint32_t)w;
+  // z ^= z >> 27
+  lo ^= umulhi32(lo, m.m32) + hi * m.m32;
+  hi ^= umulhi32(hi, m.m32);
+  const uint32_t top = umulhi32(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu;
+  return umulhi32(top, m.m24);  // top >> 8
+}
+
 // ---- magnitude rounding ---------------------------------------------------
 //
 // a = |r| where r = x * 2^s was formed in fp32; a is exact unless it fell
@@ -355,6 +399,16 @@ struct FloatParams {
   float carry;       // 2^(man+1)
   uint32_t r_exp;    // (man + 127) << 23
   int32_t tiny;      // min_exp >= 1: |x| * 2^-min_exp may flush to zero
+  int32_t ef_min;    // min_exp + 127   (scaled form, biased exponents)
+  int32_t ef_max;    // max_exp + 127
+  int32_t ef_under;  // min_exp + man + 127: underflow grid step 2^min_exp
+  int32_t sc_base;   // 254 + man
+  int32_t scaled_ok; // 2 <= exp_bits <= 7
+  uint32_t m_sh9;    // 2^9   (runtime multipliers, see RngMul)
+  uint32_t m_neg23;  // -2^23 (mod 2^32)
+  uint32_t m_pos23;  // 2^23
+  uint32_t sc_bits;  // (254 + man) << 23
+  uint32_t inv_bits; // -man << 23 (mod 2^32)
 };
 
 LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
@@ -372,6 +426,16 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.carry = u2f((uint32_t)(127 + man_bits + 1) << 23);
   p.r_exp = (uint32_t)(man_bits + 127) << 23;
   p.tiny = p.min_exp >= 1 ? 1 : 0;
+  p.ef_min = p.min_exp + 127;
+  p.ef_max = p.max_exp + 127;
+  p.ef_under = p.min_exp + man_bits + 127;
+  p.sc_base = 254 + man_bits;
+  p.scaled_ok = (exp_bits >= 2 && exp_bits <= 7) ? 1 : 0;
+  p.m_sh9 = 1u << 9;
+  p.m_neg23 = 0u - (1u << 23);
+  p.m_pos23 = 1u << 23;
+  p.sc_bits = (uint32_t)(254 + man_bits) << 23;
+  p.inv_bits = 0u - ((uint32_t)man_bits << 23);
   return p;
 }
 
@@ -422,6 +486,31 @@ LPQ_HD float quant_float_fast(float x, const FloatParams& p, uint32_t v) {
   if (sat) qb = f2u(p.max_value) | sign;
   if (k == 0.0f) qb = 0u;  // +0 for both modes
   return ab == 0u ? x : u2f(qb);
+}
+
+// Float quantizer, scaled form for NearestEven / Stochastic and
+// 2 <= exp_bits <= 7 (so every scale below is a normal fp32 power of two):
+// the binade exponent E = clamp(e, -, max_exp) (or min_exp + man below the
+// normal range, which makes the grid step 2^min_exp as in the reference's
+// two-point underflow rule) gives r = x * 2^(man - E) exactly, one rounding,
+// q = k * 2^(E - man) exactly, and saturation is a clamp to +-max_value
+// (a carry out of the top binade or e > max_exp lands beyond it).  Zero
+// results are +0 except x == -0 itself, which passes through.  About half the
+// instructions of quant_float_fast; identical results to quant_float<M>.
+template <int M>
+LPQ_HD float quant_float_scaled(float x, const FloatParams& p, uint32_t v) {
+  const uint32_t xb = f2u(x);
+  // biased exponent, (xb >> 23) & 0xFF as IMAD.HI (runtime 2^9) + LOP3
+  int ef = (int)(umulhi32(xb, p.m_sh9) & 0xFFu);
+  ef = ef < p.ef_min ? p.ef_under : (ef > p.ef_max ? p.ef_max : ef);
+  // exponent fields as IMADs against the runtime +-2^23 (FMA pipe):
+  // 2^(man - E) and 2^(E - man)
+  const float sc = u2f((uint32_t)ef * p.m_neg23 + p.sc_bits);
+  const float inv = u2f((uint32_t)ef * p.m_pos23 + p.inv_bits);
+  const float k = round_signed<M>(fmul(x, sc), v);
+  float q = fmul(k, inv);
+  q = fminf(fmaxf(q, -p.max_value), p.max_value);
+  return x == 0.0f ? x : fadd(q, 0.0f);
 }
 
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;

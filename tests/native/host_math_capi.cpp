@@ -16,7 +16,9 @@ void run(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f) {
     // the kernels' dispatch: the streaming form for even/stochastic unless
     // |x| * 2^-min_exp can flush to zero
     const lpq::FloatParams p = lpq::make_float(f->exp_bits, f->man_bits);
-    if ((M == 0 || M == 1) && !p.tiny)
+    if ((M == 0 || M == 1) && p.scaled_ok)
+      for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float_scaled<(M == 0 ? 0 : 1)>(x[i], p, v ? v[i] : 0u);
+    else if ((M == 0 || M == 1) && !p.tiny)
       for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float_fast<(M == 0 ? 0 : 1)>(x[i], p, v ? v[i] : 0u);
     else
       for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float<M>(x[i], p, v ? v[i] : 0u);
@@ -76,9 +78,13 @@ uint32_t hm_variate24(uint64_t key, uint64_t index) { return lpq::variate24(key,
 void hm_variates24(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24(key, base + (uint64_t)i);
 }
-// the kernels' pipe-balanced form (must equal variate24)
+// the kernels' pipe-balanced forms (must equal variate24)
 void hm_variates24_balanced(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24_zb(key ^ (base + (uint64_t)i), 32u);
+}
+void hm_variates24_fma(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  const lpq::RngMul m = lpq::rng_mul();
+  for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24_zf(key ^ (base + (uint64_t)i), m);
 }
 uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
 }

@@ -35,6 +35,7 @@ def hm():
     L.hm_stream_key.argtypes = [C.c_uint64, C.c_uint64]
     L.hm_variates24.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_balanced.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_variates24_fma.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     return L
 
 
@@ -79,6 +80,8 @@ def test_balanced_variate_form_is_identical(hm):
         b = np.empty(1 << 16, np.uint32)
         hm.hm_variates24(key, base, a.size, a)
         hm.hm_variates24_balanced(key, base, b.size, b)
+        assert np.array_equal(a, b)
+        hm.hm_variates24_fma(key, base, b.size, b)
         assert np.array_equal(a, b)
 
 
