@@ -34,9 +34,9 @@ HOST_MATH = os.path.join(ROOT, "build", "libquant_math_host.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
-SOURCES = ["capi.cu", "runtime.cu", "elementwise.cu", "block.cu", "gemm.cu",
-           "composed.cu"]
-HEADERS = ["quant_math.cuh", "kernels.cuh", "runtime.h"]
+SOURCES = ["capi.cu", "runtime.cu", "elementwise.cu", "block.cu",
+           "block_cluster.cu", "gemm.cu", "composed.cu"]
+HEADERS = ["quant_math.cuh", "kernels.cuh", "runtime.h", "block_common.cuh"]
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

@@ -23,68 +23,13 @@
 
 #include <algorithm>
 
+#include "block_common.cuh"
 #include "kernels.cuh"
 
 namespace lpq {
 
 namespace {
-
-constexpr uint32_t kFull = 0xFFFFFFFFu;
-
-__device__ __forceinline__ uint32_t max4(const float4& v) {
-  return max(max(absbits_for_max(v.x), absbits_for_max(v.y)),
-             max(absbits_for_max(v.z), absbits_for_max(v.w)));
-}
-__device__ __forceinline__ uint32_t nf4(const float4& v) {
-  return (nonfinite(v.x) | nonfinite(v.y) | nonfinite(v.z) | nonfinite(v.w))
-             ? 1u : 0u;
-}
-
-// TWO: the block's scales need two factors (maxima near the fp32 range
-// ends); uniform per block, so kernels branch once per block/row.
-// z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
-template <int M, bool TWO>
-__device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
-                                    float kmax, uint64_t z, const RngMul& rm) {
-  uint32_t v = 0;
-  if (M == kStochastic) v = variate24_zb(z, rm.m32);
-  if (M == kNearestEven || M == kStochastic)
-    return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
-        x, s, kmin, kmax, v);
-  return quant_block<M>(x, s, kmin, kmax, v);
-}
-
-// IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q
-template <int M, bool TWO, bool IDX4>
-__device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
-                                      float kmin, float kmax, uint64_t key,
-                                      uint64_t idx, const RngMul& m32) {
-  const uint64_t z0 = key ^ idx;
-  float4 o;
-  o.x = qb<M, TWO>(x.x, s, kmin, kmax, z0, m32);
-  o.y = qb<M, TWO>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
-  o.z = qb<M, TWO>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);
-  o.w = qb<M, TWO>(x.w, s, kmin, kmax, IDX4 ? z0 ^ 3u : key ^ (idx + 3), m32);
-  return o;
-}
-
-// |x| maximum with NaN ignored (fmaxf returns the non-NaN operand, like
-// `a > m` in reduce_max_abs); nf = x * 0 + nf turns NaN on any non-finite x.
-__device__ __forceinline__ void absmax_nf(const float4& v, float& m, float& nf) {
-  m = fmaxf(fmaxf(m, fabsf(v.x)), fmaxf(fabsf(v.y), fmaxf(fabsf(v.z), fabsf(v.w))));
-  nf = __fmaf_rn(v.x, 0.0f, nf);
-  nf = __fmaf_rn(v.y, 0.0f, nf);
-  nf = __fmaf_rn(v.z, 0.0f, nf);
-  nf = __fmaf_rn(v.w, 0.0f, nf);
-}
-
-__device__ __forceinline__ bool two_factor(const BlockScale& s) {
-  return s.s2 != 1.0f || s.o2 != 1.0f;
-}
-
-__device__ __forceinline__ void flag(uint32_t* status, uint32_t bits) {
-  if (bits) atomicOr(status, bits);
-}
+using namespace blk;
 
 // ---------------------------------------------------------------------------
 // Plan 1: one row per CTA, held in registers (single HBM pass).
@@ -172,7 +117,7 @@ void launch_rows(const float* x, float* y, int64_t L, int64_t nrows,
   if (L4 <= 128) launch_rows_t<M, 128, 1>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 256) launch_rows_t<M, 256, 1>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 512) launch_rows_t<M, 256, 2>(x, y, L, nrows, base, key, wl, st, s);
-  else if (L4 <= 1024) launch_rows_t<M, 256, 4>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 1024) launch_rows_t<M, 128, 8>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 2048) launch_rows_t<M, 512, 4>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 4096) launch_rows_t<M, 1024, 4>(x, y, L, nrows, base, key, wl, st, s);
   else launch_rows_t<M, 1024, 8>(x, y, L, nrows, base, key, wl, st, s);
@@ -395,6 +340,9 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
     launch_rows<M>(x, y, g.stride, g.extent, base, key, wl, status, s);
     return cudaGetLastError();
   }
+  if (plan == BlockPlan::kRowsCluster)
+    return launch_block_cluster(x, y, g.stride, g.extent, base, key, wl, M,
+                                status, s);
   uint32_t* maxima = static_cast<uint32_t*>(ws);
   cudaError_t e = cudaMemsetAsync(maxima, 0, sizeof(uint32_t) * g.extent, s);
   if (e != cudaSuccess) return e;
@@ -468,15 +416,16 @@ cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
 }
 
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
-  if (g.outer == 1 && g.stride % 4 == 0 && g.stride <= 32768 &&
-      g.stride >= 64 && aligned16(x) && aligned16(y))
-    return BlockPlan::kRowsInRegisters;
+  const bool rows = g.outer == 1 && g.stride % 4 == 0 && aligned16(x) && aligned16(y);
+  if (rows && g.stride <= 32768 && g.stride >= 64) return BlockPlan::kRowsInRegisters;
+  if (rows && g.stride > 32768 && cluster_size_for(g.stride) > 0)
+    return BlockPlan::kRowsCluster;
   if (g.stride >= 1024) return BlockPlan::kTwoPassSegments;
   return BlockPlan::kTwoPassColumns;
 }
 
 size_t block_workspace(const BlockGeom& g, BlockPlan p) {
-  if (p == BlockPlan::kRowsInRegisters) return 0;
+  if (block_plan_single_pass(p)) return 0;
   return (size_t)(((g.extent * 4) + 255) / 256 * 256);
 }
 

@@ -1,0 +1,69 @@
+// block_common.cuh -- device helpers shared by the block-floating-point
+// kernels (block.cu, block_cluster.cu).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace lpq {
+namespace blk {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t max4(const float4& v) {
+  return max(max(absbits_for_max(v.x), absbits_for_max(v.y)),
+             max(absbits_for_max(v.z), absbits_for_max(v.w)));
+}
+__device__ __forceinline__ uint32_t nf4(const float4& v) {
+  return (nonfinite(v.x) | nonfinite(v.y) | nonfinite(v.z) | nonfinite(v.w))
+             ? 1u : 0u;
+}
+
+// TWO: the block's scales need two factors (maxima near the fp32 range
+// ends); uniform per block, so kernels branch once per block/row.
+// z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
+template <int M, bool TWO>
+__device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
+                                    float kmax, uint64_t z, const RngMul& rm) {
+  uint32_t v = 0;
+  if (M == kStochastic) v = variate24_zb(z, rm.m32);
+  if (M == kNearestEven || M == kStochastic)
+    return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
+        x, s, kmin, kmax, v);
+  return quant_block<M>(x, s, kmin, kmax, v);
+}
+
+// IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q
+template <int M, bool TWO, bool IDX4>
+__device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
+                                      float kmin, float kmax, uint64_t key,
+                                      uint64_t idx, const RngMul& m32) {
+  const uint64_t z0 = key ^ idx;
+  float4 o;
+  o.x = qb<M, TWO>(x.x, s, kmin, kmax, z0, m32);
+  o.y = qb<M, TWO>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
+  o.z = qb<M, TWO>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);
+  o.w = qb<M, TWO>(x.w, s, kmin, kmax, IDX4 ? z0 ^ 3u : key ^ (idx + 3), m32);
+  return o;
+}
+
+// |x| maximum with NaN ignored (fmaxf returns the non-NaN operand, like
+// `a > m` in reduce_max_abs); nf = x * 0 + nf turns NaN on any non-finite x.
+__device__ __forceinline__ void absmax_nf(const float4& v, float& m, float& nf) {
+  m = fmaxf(fmaxf(m, fabsf(v.x)), fmaxf(fabsf(v.y), fmaxf(fabsf(v.z), fabsf(v.w))));
+  nf = __fmaf_rn(v.x, 0.0f, nf);
+  nf = __fmaf_rn(v.y, 0.0f, nf);
+  nf = __fmaf_rn(v.z, 0.0f, nf);
+  nf = __fmaf_rn(v.w, 0.0f, nf);
+}
+
+__device__ __forceinline__ bool two_factor(const BlockScale& s) {
+  return s.s2 != 1.0f || s.o2 != 1.0f;
+}
+
+__device__ __forceinline__ void flag(uint32_t* status, uint32_t bits) {
+  if (bits) atomicOr(status, bits);
+}
+
+
+}  // namespace blk
+}  // namespace lpq

@@ -40,11 +40,20 @@ struct BlockGeom {
 };
 
 // Which plan a block quantization uses (and how many HBM passes it makes).
-enum class BlockPlan { kRowsInRegisters, kTwoPassSegments, kTwoPassColumns };
+enum class BlockPlan { kRowsInRegisters, kRowsCluster, kTwoPassSegments,
+                       kTwoPassColumns };
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y);
 inline int block_plan_passes(BlockPlan p) {
-  return p == BlockPlan::kRowsInRegisters ? 1 : 2;
+  return (p == BlockPlan::kRowsInRegisters || p == BlockPlan::kRowsCluster) ? 1 : 2;
 }
+inline bool block_plan_single_pass(BlockPlan p) { return block_plan_passes(p) == 1; }
+// cluster plan (block_cluster.cu): CTAs per row for a contiguous block of L
+// floats, 0 if too long
+int cluster_size_for(int64_t L);
+cudaError_t launch_block_cluster(const float* x, float* y, int64_t L,
+                                 int64_t nrows, uint64_t base, uint64_t key,
+                                 int wl, int mode, uint32_t* status,
+                                 cudaStream_t s);
 // Workspace bytes for a plan: extent uint32 maxima (two-pass plans only).
 size_t block_workspace(const BlockGeom& g, BlockPlan p);
 

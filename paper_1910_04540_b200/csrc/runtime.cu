@@ -330,7 +330,7 @@ lpq_status host_context_quantize(const float* x, float* y,
     return stream_quantize(c, x, y, n, 1, false, index_base, f, mode, seed, call);
   // an aligned device buffer decides the plan exactly as the device call will
   static const float* kAligned = reinterpret_cast<const float*>(uintptr_t(256));
-  if (block_plan(g, kAligned, kAligned) == BlockPlan::kRowsInRegisters)
+  if (block_plan_single_pass(block_plan(g, kAligned, kAligned)))
     return stream_quantize(c, x, y, n, g.stride, true, index_base, f, mode,
                            seed, call);
   return resident_quantize(c, x, y, shape, rank, n, index_base, f, mode, seed,
