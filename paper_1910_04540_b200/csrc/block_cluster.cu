@@ -1,16 +1,17 @@
-// block_cluster.cu -- single-pass block floating point for long contiguous
-// blocks (32K < block <= ~900K floats, e.g. the per-sample activation blocks
-// of ResNet-50 at batch 256, up to 802,816 floats = 3.2 MB).
+// block_cluster.cu -- single-HBM-pass block floating point for long
+// contiguous blocks (> 32K floats, e.g. the per-sample activation blocks of
+// ResNet-50 at batch 256, up to 802,816 floats = 3.2 MB).
 //
-// A row (one block) is spread over a thread-block CLUSTER of CS CTAs (up to
-// 16, one per SM).  Each CTA streams its slice HBM -> shared memory with TMA
-// bulk copies (cp.async.bulk ... mbarrier::complete_tx, in chunks so the
-// max-reduction starts while later chunks are in flight), reduces the slice's
-// max|x|, publishes it in its shared memory, and after a cluster barrier
-// reads the other CTAs' maxima through distributed shared memory
-// (mapa + ld.shared::cluster).  It then quantizes its slice from shared
-// memory and streams it out.  HBM sees every element exactly once each way:
-// 8 algorithmic bytes per element instead of the two-pass plan's 12.
+// A row (one block) is spread over a thread-block CLUSTER of up to 16 CTAs.
+// Each CTA reduces max|x| over its slice, publishes it in its shared memory,
+// and after a cluster barrier reads the other CTAs' maxima through
+// distributed shared memory (mapa + ld.shared::cluster) -- no global atomics,
+// no second kernel.  It then re-reads its slice, which the residency cap keeps
+// in the 126 MB L2, and streams the quantized values out: one HBM read and one
+// HBM write per element (8 algorithmic bytes instead of the two-pass plan's
+// 12).  (A first version staged the slice in shared memory with TMA bulk
+// copies; one 196 KB CTA per SM could not overlap loading with storing and
+// reached only 4.3 TB/s -- see DESIGN.md.)
 // Semantics: fused_block (proj/src/quant_ops.cpp:68-115) with block_dim such
 // that blocks are contiguous rows.
 #include <cuda_runtime.h>
@@ -26,9 +27,10 @@ namespace {
 
 using namespace blk;
 
-constexpr int kCT = 512;            // threads per CTA
-constexpr int kChunkBytes = 32768;  // TMA bulk chunk (one mbarrier each)
-constexpr int kMaxChunks = 8;       // <= 256 KB per CTA
+constexpr int kCT = 256;          // threads per CTA
+constexpr int kU = 4;             // float4 per thread per trip
+constexpr int kCtasPerSm = 2;     // residency cap (L2 budget for rows in flight)
+constexpr int64_t kSliceTarget = 16384;  // floats per CTA (sets the cluster size)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -56,35 +58,20 @@ __device__ __forceinline__ uint32_t ld_dsmem(const uint32_t* local, uint32_t ran
   return v;
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n LPQ_CL_WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra LPQ_CL_WAIT;\n}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
-                                          uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1], %2, [%3];"
-      :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 // One cluster per row; CTA `rank` owns float4s [rank*S4, min(L4,(rank+1)*S4)).
+// Pass 1 streams the slice from HBM (normal L2 policy: it stays in L2),
+// reduces max|x| and publishes it in shared memory; after a cluster barrier
+// every CTA gathers the CS slice maxima over DSMEM; pass 2 re-reads the slice
+// (L2 hits, evict-first) and streams the quantized values out (evict-first).
+// HBM traffic: one read + one write per element (8 algorithmic bytes).  The
+// dynamic shared-memory request only caps residency at kCtasPerSm CTAs/SM so
+// the rows in flight fit in the 126 MB L2.
 template <int M, bool IDX4>
-__global__ void __launch_bounds__(kCT, 1)
+__global__ void __launch_bounds__(kCT)
     k_block_rows_cluster(const float* __restrict__ x, float* __restrict__ y,
                          int64_t L, int64_t S4, uint64_t base, uint64_t key,
                          int wl, RngMul rm, uint32_t* __restrict__ status) {
-  extern __shared__ __align__(128) float4 slice[];
-  __shared__ __align__(8) uint64_t bars[kMaxChunks];
   __shared__ uint32_t red[kCT / 32];
   __shared__ uint32_t cta_max;
   const uint32_t rank = cluster_rank();
@@ -97,32 +84,20 @@ __global__ void __launch_bounds__(kCT, 1)
   const int64_t len4 = rem4 <= 0 ? 0 : (rem4 < S4 ? rem4 : S4);
   const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + row * L) + s0;
   float4* __restrict__ yr = reinterpret_cast<float4*>(y + row * L) + s0;
-  const int64_t bytes = len4 * 16;
-  const int nchunks = (int)((bytes + kChunkBytes - 1) / kChunkBytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < nchunks; ++c) mbar_init(&bars[c], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int c = 0; c < nchunks; ++c) {
-      const int64_t off = (int64_t)c * kChunkBytes;
-      const uint32_t nb = (uint32_t)(bytes - off < kChunkBytes ? bytes - off : kChunkBytes);
-      mbar_expect_tx(&bars[c], nb);
-      bulk_load(reinterpret_cast<char*>(slice) + off,
-                reinterpret_cast<const char*>(xr) + off, nb, &bars[c]);
-    }
-  }
-  __syncthreads();
-
-  // pass over shared memory: max|x| (NaN ignored) and the non-finite probe
+  // pass 1: max|x| (NaN ignored) and the non-finite probe
   float mf = 0.0f, nf = 0.0f;
-  constexpr int kChunk4 = kChunkBytes / 16;
-  for (int c = 0; c < nchunks; ++c) {
-    mbar_wait(&bars[c], 0);
-    const int64_t ce = (int64_t)(c + 1) * kChunk4;
-    const int64_t e = len4 < ce ? len4 : ce;
-    for (int64_t j = (int64_t)c * kChunk4 + threadIdx.x; j < e; j += kCT)
-      absmax_nf(slice[j], mf, nf);
+  for (int64_t j0 = threadIdx.x; j0 < len4; j0 += (int64_t)kCT * kU) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t j = j0 + (int64_t)u * kCT;
+      if (j < len4) v[u] = __ldg(xr + j);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j0 + (int64_t)u * kCT < len4) absmax_nf(v[u], mf, nf);
   }
   uint32_t m = __reduce_max_sync(kFull, f2u(mf));
   if (lane == 0) red[warp] = m;
@@ -141,16 +116,26 @@ __global__ void __launch_bounds__(kCT, 1)
   // its maximum: arrive now, wait at the very end
   cluster_arrive();
 
+  // pass 2: quantize (the slice is L2-resident from pass 1)
   const BlockScale sc = make_block_scale(row_max, wl);
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
   const uint64_t ebase = base + (uint64_t)(row * L + s0 * 4);
-  if (!two_factor(sc)) {
-    for (int64_t j = threadIdx.x; j < len4; j += kCT)
-      __stcs(yr + j, qb4<M, false, IDX4>(slice[j], sc, kmin, kmax, key, ebase + 4 * j, rm));
-  } else {
-    for (int64_t j = threadIdx.x; j < len4; j += kCT)
-      __stcs(yr + j, qb4<M, true, IDX4>(slice[j], sc, kmin, kmax, key, ebase + 4 * j, rm));
+  const bool two = two_factor(sc);
+  for (int64_t j0 = threadIdx.x; j0 < len4; j0 += (int64_t)kCT * kU) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t j = j0 + (int64_t)u * kCT;
+      if (j < len4) v[u] = __ldcs(xr + j);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t j = j0 + (int64_t)u * kCT;
+      if (j < len4)
+        __stcs(yr + j, two ? qb4<M, true, IDX4>(v[u], sc, kmin, kmax, key, ebase + 4 * j, rm)
+                           : qb4<M, false, IDX4>(v[u], sc, kmin, kmax, key, ebase + 4 * j, rm));
+    }
   }
   uint32_t bad = (sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u);
   bad = __reduce_or_sync(kFull, bad);
@@ -164,10 +149,11 @@ cudaError_t launch_cluster_t(const float* x, float* y, int64_t L, int64_t nrows,
                              uint32_t* st, cudaStream_t s) {
   const int64_t L4 = L >> 2;
   const int64_t S4 = (L4 + cs - 1) / cs;
-  const size_t smem = (size_t)S4 * 16;
   auto kern = k_block_rows_cluster<M, IDX4>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  // residency cap: request a share of shared memory so that at most
+  // kCtasPerSm CTAs are resident per SM
+  const int smem = device_info().max_smem_optin / kCtasPerSm - 2048;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   if (cs > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -176,7 +162,7 @@ cudaError_t launch_cluster_t(const float* x, float* y, int64_t L, int64_t nrows,
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nrows * cs), 1, 1);
   cfg.blockDim = dim3(kCT, 1, 1);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -201,16 +187,12 @@ cudaError_t launch_cluster_m(const float* x, float* y, int64_t L, int64_t nrows,
 
 }  // namespace
 
-// Cluster size for a contiguous block of L floats, or 0 if the cluster plan
-// does not apply (slices of at most kMaxChunks * kChunkBytes per CTA, at most
-// 16 CTAs).
+// Cluster size for a contiguous block of L floats: ~kSliceTarget floats per
+// CTA, at most 16 CTAs (non-portable cluster size); any L is accepted (very
+// long rows simply have longer slices, and stop fitting in L2).
 int cluster_size_for(int64_t L) {
-  const int64_t max_slice = (int64_t)kMaxChunks * kChunkBytes / 4;  // floats
-  const int64_t cap = std::min<int64_t>(max_slice,
-                                        (int64_t)(device_info().max_smem_optin - 4096) / 16 * 4);
-  for (int cs = 1; cs <= 16; ++cs)
-    if ((L + cs - 1) / cs <= cap) return cs;
-  return 0;
+  const int64_t cs = (L + kSliceTarget - 1) / kSliceTarget;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(16, cs));
 }
 
 cudaError_t launch_block_cluster(const float* x, float* y, int64_t L,
