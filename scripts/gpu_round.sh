@@ -5,7 +5,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; 
 if [ "${TESTS:-1}" = 1 ]; then
   timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.txt
 fi
-for c in c2 c3 c3s c1 c1n; do
+for c in c2 c3 c3s c1 c1n c1big c5; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 5 $( [ $c != c2 ] && echo --no-e2e --no-cpu ) > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 timeout 300 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
@@ -24,6 +24,6 @@ if [ "${NCU:-1}" = 1 ]; then
       --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_launches.log 2>&1
 fi
 tail -3 gpurun_out/pytest_gpu.txt 2>/dev/null
-for c in c2 c3 c3s c1 c1n c4; do python -c "
+for c in c2 c3 c3s c1 c1n c1big c5 c4; do python -c "
 import json; d=json.load(open('gpurun_out/bench_$c.json')); r=d['roofline']
 print('$c', d['value'], d['unit'], 'frac', r['frac'], 'e2e', (d.get('e2e') or {}).get('value'), 'cpu', (d.get('cpu_baseline') or {}).get('value'), d['clocks']['sm_mhz'], d['clocks']['reasons'])" 2>&1 | tail -1; done
