@@ -297,8 +297,14 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the host entry point (pinned host buffers) -----------------
     e2e = None
     if not args.no_e2e:
-        hx = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        hy = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        host_mem = "pinned"
+        try:
+            hx = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+            hy = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        except RuntimeError:  # not enough page-lockable memory: pageable path
+            host_mem = "pageable"
+            hx = torch.empty(shape, dtype=torch.float32)
+            hy = torch.empty(shape, dtype=torch.float32)
         hx.copy_(xs[0])
         e_steps = max(1, min(args.steps, args.e2e_steps))
 
@@ -324,7 +330,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": round(bytes_per_rank_step * world * e_steps / et / 1e9, 3),
                "unit": "GB/s", "h2d_bytes_per_step": 4 * n * world,
                "d2h_bytes_per_step": 4 * n * world, "steps": e_steps,
-               "api": "lpq_quantize_host (include/lpq.h), pinned host buffers"}
+               "api": f"lpq_quantize_host (include/lpq.h), {host_mem} host buffers"}
         del hx, hy
     # ---- roofline of the dominant kernel --------------------------------------------
     peak, peak_src, peaks = load_peaks()
@@ -432,6 +438,60 @@ def run_gemm(args, rank, world, local_rank):
                      "peak": round(peak_t, 2), "unit": "TFLOP/s",
                      "frac": round(ach / peak_t, 4), "traffic": None,
                      "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz"},
+        "clocks": clk.summary(),
+    }
+
+
+# ---------------------------------------------------------------------------
+def run_matmul_q(args, rank, world, local_rank):
+    """The reference's quantized_matmul (quant_ops.cpp:191-193) at 4096^3:
+    double-accumulated matmul in ascending k with fixed(8,4) stochastic
+    quantization fused into the epilogue (lpq_matmul_q, DFMA)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1910_04540_b200 as q
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    M = N = K = 4096
+    a = q.random_uniform((M, K), 41, 0, -1.0, 1.0, device=dev, index_base=rank * M * K)
+    b = q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev)
+    c = torch.empty((M, N), device=dev)
+    spec = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, SEED)
+    for _ in range(args.warmup):
+        q.quantized_matmul_at(a, b, spec, 0, out=c, sync=False, row_base=rank * M)
+    q.fetch_status(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = q.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t0.record(s)
+        for _ in range(args.steps):
+            q.quantized_matmul_at(a, b, spec, 0, out=c, sync=False, row_base=rank * M)
+        t1.record(s)
+        torch.cuda.synchronize()
+    q.fetch_status(dev)
+    el = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    flops = 2.0 * M * N * K
+    ach = flops * args.steps / el / 1e12
+    return {
+        "metric": "reference quantized_matmul GFLOP/s (double accumulation, fused quantize epilogue)",
+        "value": round(flops * world * args.steps / el / 1e9, 1), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp64 accumulate, fp32 I/O",
+        "data": "synthetic", "config": {"workload": "quantized_matmul 4096^3, fixed(8,4) stochastic",
+                                        "parallelism": f"shard{world}"},
+        "gpu_launches": q.launch_count() - l0,
+        "roofline": {"bound": "fp64", "achieved": round(ach, 2), "unit": "TFLOP/s",
+                     "peak": None, "frac": None, "traffic": None,
+                     "peak_source": "no measured FP64 peak in MEASURED_PEAKS.json"},
         "clocks": clk.summary(),
     }
 
@@ -602,7 +662,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c4ref", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
@@ -614,7 +674,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        if args.config in ("c4", "c5"):
+        if args.config in ("c4", "c4ref", "c5"):
             args.config = "c2"
         out = run_reference(args, rank, world)
         if out is not None:
@@ -625,7 +685,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    runner = {"c4": run_gemm, "c5": run_sweep}.get(args.config, run_ours)
+    runner = {"c4": run_gemm, "c4ref": run_matmul_q, "c5": run_sweep}.get(args.config, run_ours)
     out = runner(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -172,6 +172,31 @@ lpq_status lpq_quantize_composed(const float* x, float* y, const int64_t* shape,
                                  uint64_t call, void* ws, size_t ws_bytes,
                                  uint32_t* d_status, void* stream);
 
+/* One quantizer of a fused multi-quantizer kernel: a (non-block) format, a
+ * rounding mode and the RngStream (seed, call) its variates come from. */
+typedef struct {
+  lpq_format format;
+  int32_t mode;
+  int32_t enabled;  /* 0: keep full precision (an absent QuantConfig slot) */
+  uint64_t seed;
+  uint64_t call;
+} lpq_quant_slot;
+
+/* LowPrecisionOptimizer::step for ONE parameter tensor (proj/src/train.cpp:
+ * 148-178) fused into one pass over n elements (device pointers):
+ *   g = Qg(grad);  vel = Qv(fl32(fl32(momentum*vel) + g));
+ *   acc = Qa(fl32(acc - fl32(lr*vel)));  weight = Qw(acc)
+ * Qv and Qa are the reference's two accumulator quantizations (the same
+ * spec used twice: call ids c and c+1 when stochastic).  Variates use flat
+ * index index_base + i.  Block formats -> LPQ_ERR_UNSUPPORTED. */
+lpq_status lpq_sgd_step(const float* grad, float* vel, float* acc,
+                        float* weight, int64_t n, float momentum, float lr,
+                        const lpq_quant_slot* grad_q,
+                        const lpq_quant_slot* acc_q_vel,
+                        const lpq_quant_slot* acc_q_acc,
+                        const lpq_quant_slot* weight_q, uint64_t index_base,
+                        uint32_t* d_status, void* stream);
+
 /* ---- host entry points (synchronous; host buffers) ---------------------- */
 
 /* quantize_fused_at over host memory on CUDA device `device` (-1 = current):

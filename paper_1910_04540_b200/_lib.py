@@ -63,7 +63,14 @@ _EXC = {
     ERR_INVALID_VALUE: InvalidValueError,
 }
 
+class LpqQuantSlot(C.Structure):
+    """lpq_quant_slot (include/lpq.h)."""
+    _fields_ = [("format", LpqFormat), ("mode", C.c_int32), ("enabled", C.c_int32),
+                ("seed", C.c_uint64), ("call", C.c_uint64)]
+
+
 _F = C.POINTER(LpqFormat)
+_S = C.POINTER(LpqQuantSlot)
 _I64P = C.POINTER(C.c_int64)
 _VP = C.c_void_p
 
@@ -109,6 +116,9 @@ _PROTOS = {
     "lpq_quantize_composed_host": (C.c_int, [_VP, _VP, _I64P, C.c_int,
                                              C.c_uint64, _F, C.c_int,
                                              C.c_uint64, C.c_uint64, C.c_int]),
+    "lpq_sgd_step": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, C.c_float,
+                               C.c_float, _S, _S, _S, _S, C.c_uint64, _VP,
+                               _VP]),
     "lpq_shutdown": (None, []),
 }
 

@@ -1,0 +1,141 @@
+// optim.cu -- the low-precision optimizer step, fused (SURVEY.md §8(f) row 2:
+// the training-loop caller of the quantizers).
+//
+// Reference: LowPrecisionOptimizer::step (proj/src/train.cpp:148-178).  Per
+// parameter tensor it makes four quantize_fused calls (gradient, velocity,
+// accumulator, weight) and four elementwise tensor ops (scale, add, scale,
+// sub), each a full pass with its own temporary.  Here the whole update of
+// one parameter is ONE kernel pass: read g, vel, acc once, write vel, acc, w
+// once (24 algorithmic bytes per element), with the reference's per-op fp32
+// arithmetic (`float(double(a) op double(b))` == fp32 RN) and its four
+// quantizers (each with its own seed and call id, flat-index variates):
+//
+//   g   = Qg(g)
+//   v   = Qa1(fl32(fl32(momentum * vel) + g));   vel = v
+//   a   = Qa2(fl32(acc - fl32(lr * v)));         acc = a
+//   w   = Qw(a)
+//
+// Block formats need a whole-tensor maximum of an intermediate and cannot be
+// fused; they are rejected (LPQ_ERR_UNSUPPORTED) -- run the unfused sequence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../../include/lpq.h"
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace lpq {
+
+namespace {
+
+constexpr int kT = 256;
+
+struct Slot {
+  int32_t enabled;
+  int32_t kind;  // LPQ_FLOAT / LPQ_FIXED
+  int32_t mode;
+  int32_t saturate;
+  uint64_t key;
+  FloatParams fp;
+  FixedParams xp;
+};
+
+template <int M>
+__device__ __forceinline__ float q_mode(float x, const Slot& s, uint32_t v) {
+  if (s.kind == LPQ_FLOAT) return quant_float<M>(x, s.fp, v);
+  if (s.saturate) return quant_fixed<M, true>(x, s.xp, v);
+  return quant_fixed<M, false>(x, s.xp, v);
+}
+
+// grid-uniform dispatch on the slot's mode (no divergence)
+__device__ __forceinline__ float q_slot(float x, const Slot& s, uint64_t idx,
+                                        uint32_t& flags) {
+  if (!s.enabled) return x;
+  if (nonfinite(x)) flags |= kStatusNonFinite;
+  switch (s.mode) {
+    case kStochastic: return q_mode<kStochastic>(x, s, variate24(s.key, idx));
+    case kNearestAway: return q_mode<kNearestAway>(x, s, 0u);
+    case kNearestZero: return q_mode<kNearestZero>(x, s, 0u);
+    default: return q_mode<kNearestEven>(x, s, 0u);
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+    k_sgd_step(const float* __restrict__ grad, float* __restrict__ vel,
+               float* __restrict__ acc, float* __restrict__ w, int64_t n,
+               float momentum, float lr, Slot qg, Slot qa1, Slot qa2, Slot qw,
+               uint64_t base, uint32_t* __restrict__ status) {
+  uint32_t flags = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kT) {
+    const uint64_t idx = base + (uint64_t)i;
+    const float g = q_slot(grad[i], qg, idx, flags);
+    float v = __fadd_rn(__fmul_rn(momentum, vel[i]), g);  // add(scale(vel, m), g)
+    if (nonfinite(v)) flags |= kStatusInvalidValue;        // map_elements check
+    v = q_slot(v, qa1, idx, flags);
+    vel[i] = v;
+    const float lv = __fmul_rn(v, lr);                      // scale(v, lr)
+    float a = __fsub_rn(acc[i], lv);                        // sub(acc, .)
+    if (nonfinite(lv) || nonfinite(a)) flags |= kStatusInvalidValue;
+    a = q_slot(a, qa2, idx, flags);
+    acc[i] = a;
+    w[i] = q_slot(a, qw, idx, flags);
+  }
+  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
+}
+
+lpq_status make_slot(const lpq_quant_slot* in, Slot* out) {
+  *out = Slot{};
+  if (!in || !in->enabled) return LPQ_OK;
+  lpq_status st = check_format(&in->format);
+  if (st != LPQ_OK) return st;
+  if (in->format.kind == LPQ_BLOCK) return LPQ_ERR_UNSUPPORTED;
+  if (in->mode < 0 || in->mode > 3) return LPQ_ERR_ARGUMENT;
+  out->enabled = 1;
+  out->kind = in->format.kind;
+  out->mode = in->mode;
+  out->saturate = in->format.saturate;
+  out->key = stream_key(in->seed, in->call);
+  if (in->format.kind == LPQ_FLOAT)
+    out->fp = make_float(in->format.exp_bits, in->format.man_bits);
+  else
+    out->xp = make_fixed(in->format.wl, in->format.fl, in->format.symmetric != 0,
+                         in->format.saturate != 0);
+  return LPQ_OK;
+}
+
+}  // namespace
+
+}  // namespace lpq
+
+using namespace lpq;
+
+extern "C" lpq_status lpq_sgd_step(const float* grad, float* vel, float* acc,
+                                   float* weight, int64_t n, float momentum,
+                                   float lr, const lpq_quant_slot* grad_q,
+                                   const lpq_quant_slot* acc_q_vel,
+                                   const lpq_quant_slot* acc_q_acc,
+                                   const lpq_quant_slot* weight_q,
+                                   uint64_t index_base, uint32_t* d_status,
+                                   void* stream) {
+  if (n < 0) return LPQ_ERR_ARGUMENT;
+  Slot s[4];
+  const lpq_quant_slot* in[4] = {grad_q, acc_q_vel, acc_q_acc, weight_q};
+  for (int k = 0; k < 4; ++k) {
+    lpq_status st = make_slot(in[k], &s[k]);
+    if (st != LPQ_OK) return st;
+  }
+  if (n == 0) return LPQ_OK;
+  if (!grad || !vel || !acc || !weight || !d_status) return LPQ_ERR_ARGUMENT;
+  const int64_t cap = (int64_t)device_info().sm_count * 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (n + kT - 1) / kT));
+  k_sgd_step<<<grid, kT, 0, static_cast<cudaStream_t>(stream)>>>(
+      grad, vel, acc, weight, n, momentum, lr, s[0], s[1], s[2], s[3], index_base,
+      d_status);
+  note_launch();
+  note_passes(1);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
+}

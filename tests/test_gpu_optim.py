@@ -1,0 +1,109 @@
+"""Fused low-precision optimizer step (lpq_sgd_step) vs a restatement of
+LowPrecisionOptimizer::step (proj/src/train.cpp:148-178) built from the
+oracle's quantizer and numpy fp32 ops (IEEE RN, == float(double op double)).
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import STOCHASTIC, bits, fixed_fmt, float_fmt
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def oracle_fmt(f):
+    import paper_1910_04540_b200 as q
+    if isinstance(f, q.FloatFormat):
+        return float_fmt(f.exp_bits, f.man_bits)
+    return fixed_fmt(f.wl, f.fl, f.symmetric, f.saturate)
+
+
+class RefOpt:
+    """train.cpp:148-178, elementwise formats, numpy + oracle."""
+
+    def __init__(self, oracle, params, lr, mom, w, a, g):
+        self.o, self.lr, self.mom = oracle, np.float32(lr), np.float32(mom)
+        self.specs = {"w": w, "a": a, "g": g}
+        self.calls = {"w": w.call_counter if w else 0, "a": a.call_counter if a else 0,
+                      "g": g.call_counter if g else 0}
+        self.acc = [p.copy() for p in params]
+        self.vel = [np.zeros_like(p) for p in params]
+
+    def q(self, which, x):
+        s = self.specs[which]
+        if s is None:
+            return x
+        st, y = self.o.quantize(x, oracle_fmt(s.format), int(s.mode), seed=s.seed,
+                                call=self.calls[which])
+        assert st == 0
+        if int(s.mode) == STOCHASTIC:
+            self.calls[which] += 1
+        return y
+
+    def step(self, params, grads):
+        out = []
+        for i, (p, g) in enumerate(zip(params, grads)):
+            g = self.q("g", g)
+            v = (self.vel[i] * self.mom).astype(np.float32) + g
+            v = self.q("a", v.astype(np.float32))
+            self.vel[i] = v
+            a = (self.acc[i] - (v * self.lr).astype(np.float32)).astype(np.float32)
+            a = self.q("a", a)
+            self.acc[i] = a
+            out.append(self.q("w", a))
+        return out
+
+
+@pytest.mark.parametrize("cfg", ["wage_like", "float_all_stoch", "no_quant", "nearest_away"])
+def test_sgd_step_matches_reference_semantics(oracle, cfg):
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200.optim import LowPrecisionOptimizer
+    S, E = q.RoundingMode.Stochastic, q.RoundingMode.NearestEven
+    specs = {
+        "wage_like": dict(weight=q.QuantSpec(q.FixedFormat(8, 6), E),
+                          accumulator=q.QuantSpec(q.FixedFormat(16, 12), S, 11),
+                          gradient=q.QuantSpec(q.FixedFormat(8, 10), S, 12)),
+        "float_all_stoch": dict(weight=q.QuantSpec(q.FloatFormat(5, 2), S, 1),
+                                accumulator=q.QuantSpec(q.FloatFormat(8, 7), S, 2, 5),
+                                gradient=q.QuantSpec(q.FloatFormat(4, 3), S, 3)),
+        "no_quant": dict(),
+        "nearest_away": dict(weight=q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode.NearestAway),
+                             gradient=q.QuantSpec(q.FixedFormat(6, 4, True, False),
+                                                  q.RoundingMode.NearestTowardZero)),
+    }[cfg]
+    rng = np.random.default_rng(5)
+    shapes = [(64, 33), (33,), (10, 64), (10,)]
+    params = [rng.uniform(-0.5, 0.5, s).astype(np.float32) for s in shapes]
+    dev_params = [torch.from_numpy(p.copy()).cuda() for p in params]
+    opt = LowPrecisionOptimizer(dev_params, lr=0.05, momentum=0.9, **specs)
+    import copy
+    ref = RefOpt(oracle, params, 0.05, 0.9, copy.deepcopy(specs.get("weight")),
+                 copy.deepcopy(specs.get("accumulator")), copy.deepcopy(specs.get("gradient")))
+    host_params = params
+    for step in range(4):
+        grads = [rng.normal(0, 0.1, s).astype(np.float32) for s in shapes]
+        host_params = ref.step(host_params, grads)
+        opt.step([torch.from_numpy(g).cuda() for g in grads])
+        for hp, dp in zip(host_params, dev_params):
+            assert np.array_equal(bits(hp), bits(dp.cpu().numpy())), (cfg, step)
+        for ha, da in zip(ref.acc, opt.accumulators()):
+            assert np.array_equal(bits(ha), bits(da.cpu().numpy()))
+    for k, spec in (("w", opt.weight_spec), ("a", opt.acc_spec), ("g", opt.grad_spec)):
+        if spec is not None:
+            assert spec.call_counter == ref.calls[k]
+
+
+def test_sgd_step_rejects_block_and_bad_args():
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200.optim import LowPrecisionOptimizer
+    p = [torch.zeros(8, device="cuda")]
+    with pytest.raises(q.FormatError):
+        LowPrecisionOptimizer(p, lr=-1.0, momentum=0.5)
+    with pytest.raises(q.FormatError):
+        LowPrecisionOptimizer(p, lr=0.1, momentum=1.0)
+    opt = LowPrecisionOptimizer(p, lr=0.1, momentum=0.5,
+                                weight=q.QuantSpec(q.BlockFloatFormat(8)))
+    with pytest.raises(q.UnsupportedFormatError):
+        opt.step([torch.ones(8, device="cuda")])
+    with pytest.raises(q.ShapeError):
+        LowPrecisionOptimizer(p, 0.1, 0.5).step([torch.ones(9, device="cuda")])
