@@ -523,23 +523,49 @@ def run_sweep(args, rank, world, local_rank):
                         q.RoundingMode.Stochastic))
         tensors.append((q.random_uniform(ashape, 300 + i, 0, -4.0, 4.0, device=dev),
                         q.RoundingMode.NearestEven))
-    out = torch.empty(max(t.numel() for t, _ in tensors), device=dev)
+    outs = [torch.empty_like(t) for t, _ in tensors]  # weights/grads outputs
+    out_big = torch.empty(max(t.numel() for t, _ in tensors), device=dev)
     ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
     status = q.quant._status_buf(dev)
-    calls = []
-    for t, mode in tensors:
+    # weights and gradients: one grouped launch per (kind, format) --
+    # lpq_quantize_grouped, 54 tensors each; activations: one launch each
+    groups, singles, keep = [], [], []
+    for kind in (0, 1):  # 0 weights (nearest), 1 gradients (stochastic)
+        idx = list(range(kind, len(tensors), 3))
+        for f in fmts:
+            descs = (_lib.LpqTensorDesc * len(idx))()
+            for j, i in enumerate(idx):
+                t = tensors[i][0]
+                shp = _lib.shape_array(t.shape)
+                keep.append(shp)
+                descs[j] = _lib.LpqTensorDesc(t.data_ptr(), outs[i].data_ptr(), shp,
+                                              t.dim(), 0, 0, j)
+            groups.append((descs, len(idx), f.c(), int(tensors[kind][1]),
+                           sum(tensors[i][0].numel() for i in idx)))
+    for t, mode in tensors[2::3]:
         shp = _lib.shape_array(t.shape)
         for f in fmts:
-            calls.append((C.c_void_p(t.data_ptr()), C.c_void_p(out.data_ptr()), shp,
-                          t.dim(), f.c(), int(mode), t.numel()))
+            singles.append((C.c_void_p(t.data_ptr()), C.c_void_p(out_big.data_ptr()), shp,
+                            t.dim(), f.c(), int(mode), t.numel()))
+
+    def run_group(g, sp):
+        descs, cnt, fc, mode, n = g
+        _lib.check(_lib.lib.lpq_quantize_grouped(descs, cnt, C.byref(fc), mode, SEED,
+                                                 C.c_void_p(ws.data_ptr()), ws.numel(),
+                                                 C.c_void_p(status.data_ptr()), sp), "sweep")
+
+    def run_single(c, sp):
+        xp, yp, shp, rank_, fc, mode, n = c
+        _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode, SEED, 0,
+                                         C.c_void_p(ws.data_ptr()), ws.numel(),
+                                         C.c_void_p(status.data_ptr()), sp), "sweep")
 
     def sweep(stream):
         sp = C.c_void_p(stream.cuda_stream)
-        for xp, yp, shp, rank_, fc, mode, n in calls:
-            _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode,
-                                             SEED, 0, C.c_void_p(ws.data_ptr()),
-                                             ws.numel(), C.c_void_p(status.data_ptr()),
-                                             sp), "sweep")
+        for g in groups:
+            run_group(g, sp)
+        for c in singles:
+            run_single(c, sp)
 
     # algorithmic bytes from the passes the library makes (8 B/elem single
     # pass, 12 B/elem two-pass block plans)
@@ -547,14 +573,16 @@ def run_sweep(args, rank, world, local_rank):
     l0 = q.launch_count()
     nbytes = 0
     s0 = torch.cuda.current_stream(dev)
-    for xp, yp, shp, rank_, fc, mode, n in calls:
+    sp0 = C.c_void_p(s0.cuda_stream)
+    for g in groups:
+        run_group(g, sp0)
+        nbytes += 8 * g[4]
+    for c in singles:
         p0 = q.pass_count()
-        _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode, SEED, 0,
-                                         C.c_void_p(ws.data_ptr()), ws.numel(),
-                                         C.c_void_p(status.data_ptr()),
-                                         C.c_void_p(s0.cuda_stream)))
-        nbytes += (8 if q.pass_count() - p0 == 1 else 12) * n
+        run_single(c, sp0)
+        nbytes += (8 if q.pass_count() - p0 == 1 else 12) * c[6]
     launches_per_sweep = q.launch_count() - l0
+    calls = [None] * (3 * len(tensors))
     q.fetch_status(dev)
     g = torch.cuda.CUDAGraph()
     side = torch.cuda.Stream(dev)

@@ -172,6 +172,27 @@ lpq_status lpq_quantize_composed(const float* x, float* y, const int64_t* shape,
                                  uint64_t call, void* ws, size_t ws_bytes,
                                  uint32_t* d_status, void* stream);
 
+/* One tensor of a grouped quantization. */
+typedef struct {
+  const float* x;        /* device input  */
+  float* y;              /* device output (may equal x) */
+  const int64_t* shape;  /* host array of rank extents */
+  int32_t rank;
+  int32_t reserved;
+  uint64_t index_base;   /* flat index of x[0] (RNG counter offset) */
+  uint64_t call;         /* this tensor's call id */
+} lpq_tensor_desc;
+
+/* quantize_fused_at over many tensors with one format/mode/seed and a call
+ * id per tensor (the reference's sequence of quantize_fused calls, each
+ * advancing the counter): up to 64 tensors per kernel launch for float and
+ * fixed formats and for block formats along dim 0 with rows <= 8192 floats;
+ * other block layouts run per tensor (ws: the largest lpq_workspace_size). */
+lpq_status lpq_quantize_grouped(const lpq_tensor_desc* tensors, int count,
+                                const lpq_format* f, int mode, uint64_t seed,
+                                void* ws, size_t ws_bytes, uint32_t* d_status,
+                                void* stream);
+
 /* One quantizer of a fused multi-quantizer kernel: a (non-block) format, a
  * rounding mode and the RngStream (seed, call) its variates come from. */
 typedef struct {

@@ -69,6 +69,14 @@ class LpqQuantSlot(C.Structure):
                 ("seed", C.c_uint64), ("call", C.c_uint64)]
 
 
+class LpqTensorDesc(C.Structure):
+    """lpq_tensor_desc (include/lpq.h)."""
+    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p),
+                ("shape", C.POINTER(C.c_int64)), ("rank", C.c_int32),
+                ("reserved", C.c_int32), ("index_base", C.c_uint64),
+                ("call", C.c_uint64)]
+
+
 _F = C.POINTER(LpqFormat)
 _S = C.POINTER(LpqQuantSlot)
 _I64P = C.POINTER(C.c_int64)
@@ -119,6 +127,9 @@ _PROTOS = {
     "lpq_sgd_step": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, C.c_float,
                                C.c_float, _S, _S, _S, _S, C.c_uint64, _VP,
                                _VP]),
+    "lpq_quantize_grouped": (C.c_int, [C.POINTER(LpqTensorDesc), C.c_int, _F,
+                                       C.c_int, C.c_uint64, _VP, C.c_size_t,
+                                       _VP, _VP]),
     "lpq_shutdown": (None, []),
 }
 

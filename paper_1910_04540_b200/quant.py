@@ -274,6 +274,42 @@ def quantize_composed(t, spec: QuantSpec, **kw):
     return out
 
 
+def quantize_fused_many(tensors, spec: QuantSpec, *, outs=None, sync=True):
+    """quantize_fused over a list of CUDA tensors, in order (the call counter
+    advances once per tensor for stochastic rounding, as a loop of
+    quantize_fused calls would), in as few launches as possible
+    (lpq_quantize_grouped: up to 64 tensors per launch)."""
+    if not tensors:
+        return []
+    xs = [t.contiguous() for t in tensors]
+    ys = [torch.empty_like(x) for x in xs] if outs is None else list(outs)
+    dev = xs[0].device
+    stoch = spec.mode == RoundingMode.Stochastic
+    descs = (_lib.LpqTensorDesc * len(xs))()
+    keep = []
+    ws_need = 0
+    fmt = spec.format.c()
+    for i, (x, y) in enumerate(zip(xs, ys)):
+        shp = shape_array(x.shape)
+        keep.append(shp)
+        ws_need = max(ws_need, lib.lpq_workspace_size(C.byref(fmt), shp, x.dim()))
+        descs[i] = _lib.LpqTensorDesc(x.data_ptr(), y.data_ptr(), shp, x.dim(), 0,
+                                      0, spec.call_counter + (i if stoch else 0))
+    ws = _workspace(dev, ws_need)
+    with torch.cuda.device(dev):
+        st = lib.lpq_quantize_grouped(descs, len(xs), C.byref(fmt), int(spec.mode),
+                                      int(spec.seed),
+                                      C.c_void_p(ws.data_ptr() if ws is not None else 0),
+                                      ws_need, C.c_void_p(_status_buf(dev).data_ptr()),
+                                      _stream_ptr(dev))
+        check(st, "quantize_grouped")
+        if sync:
+            fetch_status(dev)
+    if stoch:
+        spec.call_counter += len(xs)
+    return ys
+
+
 def quantized_op(op, spec: QuantSpec):
     """quantized_op (quant_ops.hpp:36-42): quantize_fused appended to op."""
     def run(*args, **kwargs):
@@ -409,7 +445,8 @@ def variate_tensor(shape, seed: int, call: int, *, device="cuda",
 __all__ = [
     "RoundingMode", "FloatFormat", "FixedFormat", "BlockFloatFormat",
     "NumberFormat", "QuantSpec", "validate", "quantize_fused",
-    "quantize_fused_at", "quantize_composed", "quantize_composed_at",
+    "quantize_fused_at", "quantize_fused_many", "quantize_composed",
+    "quantize_composed_at",
     "quantized_op", "quantized_matmul",
     "quantized_matmul_at", "quant_gemm", "random_uniform", "variate_tensor",
     "pass_count", "reset_pass_count", "launch_count", "fetch_status",

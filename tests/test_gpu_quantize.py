@@ -313,3 +313,25 @@ def test_c3_block_rows_65536x4096(q, oracle):
         k = y / torch.exp2((ex - 1 - 6).float())
         assert torch.equal(k, torch.round(k))
         assert float(k.min()) >= -128 and float(k.max()) <= 127
+
+
+# ---- grouped (multi-tensor) quantization --------------------------------------
+@pytest.mark.parametrize("fmt_ctor,mode", [
+    (lambda q: q.FixedFormat(8, 4), STOCHASTIC), (lambda q: q.FloatFormat(5, 2), NEAREST_EVEN),
+    (lambda q: q.FloatFormat(8, 7), STOCHASTIC), (lambda q: q.BlockFloatFormat(8, 0), STOCHASTIC),
+    (lambda q: q.BlockFloatFormat(6, 0), NEAREST_EVEN), (lambda q: q.BlockFloatFormat(8, 1), NEAREST_EVEN),
+    (lambda q: q.BlockFloatFormat(8), STOCHASTIC)])
+def test_grouped_equals_sequential(q, fmt_ctor, mode):
+    fmt = fmt_ctor(q)
+    rng = np.random.default_rng(99)
+    shapes = [(64, 3, 7, 7), (256, 64, 1, 1), (10, 147), (1000, 2048), (3,), (7, 5),
+              (128, 128, 3, 3)] * 12  # 84 tensors -> two launches of <= 64
+    ts = [dev(rng.uniform(-3, 3, s).astype(np.float32) * np.float32(2.0 ** rng.integers(-8, 8)))
+          for s in shapes]
+    spec_a = q.QuantSpec(fmt, q.RoundingMode(mode), 17, 4)
+    spec_b = q.QuantSpec(fmt, q.RoundingMode(mode), 17, 4)
+    got = q.quantize_fused_many(ts, spec_a)
+    want = [q.quantize_fused(t, spec_b) for t in ts]
+    assert spec_a.call_counter == spec_b.call_counter
+    for g, w in zip(got, want):
+        assert torch.equal(g.view(torch.int32), w.view(torch.int32))
