@@ -326,6 +326,8 @@ def test_grouped_equals_sequential(q, fmt_ctor, mode):
     rng = np.random.default_rng(99)
     shapes = [(64, 3, 7, 7), (256, 64, 1, 1), (10, 147), (1000, 2048), (3,), (7, 5),
               (128, 128, 3, 3)] * 12  # 84 tensors -> two launches of <= 64
+    if getattr(fmt, "block_dim", None) == 1:
+        shapes = [s for s in shapes if len(s) >= 2]
     ts = [dev(rng.uniform(-3, 3, s).astype(np.float32) * np.float32(2.0 ** rng.integers(-8, 8)))
           for s in shapes]
     spec_a = q.QuantSpec(fmt, q.RoundingMode(mode), 17, 4)
