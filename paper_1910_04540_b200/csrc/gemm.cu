@@ -357,9 +357,12 @@ void launch_general(const float* A, const float* B, float* C, int64_t M,
 
 // ---------------------------------------------------------------------------
 // k_matmul_q: the reference quantized_matmul, DFMA accumulation in ascending
-// k with the quantizer in the epilogue.  64x64 tile, 256 threads, 4x4 double
-// accumulators per thread, A/B staged as double in shared memory.
-constexpr int kDM = 64, kDN = 64, kDK = 16, kDT = 256;
+// k with the quantizer in the epilogue.  128x128 CTA tile, 256 threads, 8x8
+// double accumulators per thread (rows ty*4+{0..3} and 64+ty*4+{0..3}, same
+// for columns, so a warp's shared-memory reads are contiguous), K staged by 8
+// as double in double-buffered shared memory, the next tile's global loads
+// issued before the current tile's math.
+constexpr int kDM = 128, kDN = 128, kDK = 8, kDT = 256;
 
 struct EpilogueFloat {
   FloatParams p;
@@ -393,47 +396,79 @@ __global__ void __launch_bounds__(kDT)
                float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                int64_t row_base, Epi epi, uint64_t key,
                uint32_t* __restrict__ status) {
-  __shared__ double As[kDK][kDM];
-  __shared__ double Bs[kDK][kDN];
+  __shared__ __align__(16) double As[2][kDK][kDM];
+  __shared__ __align__(16) double Bs[2][kDK][kDN];
   const int t = threadIdx.x;
   const int tx = t & 15, ty = t >> 4;
   const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
-  double acc[4][4];
+  double acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (int64_t k0 = 0; k0 < K; k0 += kDK) {
-    for (int e = t; e < kDM * kDK; e += kDT) {
-      const int r = e / kDK, c = e % kDK;
-      const int64_t gr = m0 + r, gc = k0 + c;
-      As[c][r] = (gr < M && gc < K) ? (double)A[gr * K + gc] : 0.0;
-      const int kr = e / kDN, nc = e % kDN;
-      const int64_t gk = k0 + kr, gn = n0 + nc;
-      Bs[kr][nc] = (gk < K && gn < N) ? (double)B[gk * N + gn] : 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  // global -> register staging: A row (t>>1), k half (t&1)*4; B k-row (t>>5),
+  // columns (t&31)*4
+  float ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+    const int64_t ar = m0 + (t >> 1), ak = k0 + (t & 1) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      ra[q] = (ar < M && ak + q < K) ? __ldg(A + ar * K + ak + q) : 0.0f;
+    const int64_t bk = k0 + (t >> 5), bn = n0 + (t & 31) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      rb[q] = (bk < K && bn + q < N) ? __ldg(B + bk * N + bn + q) : 0.0f;
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) As[buf][(t & 1) * 4 + q][t >> 1] = (double)ra[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Bs[buf][t >> 5][(t & 31) * 4 + q] = (double)rb[q];
+  };
+  const int64_t nk = (K + kDK - 1) / kDK;
+  load(0);
+  stash(0);
+  __syncthreads();
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < nk) load((kt + 1) * kDK);
+    const int kk_end = (int)min((int64_t)kDK, K - kt * kDK);
+    auto step = [&](int kk) {
+      double a[8], b[8];
+      const double2* ap0 = reinterpret_cast<const double2*>(&As[buf][kk][ty * 4]);
+      const double2* ap1 = reinterpret_cast<const double2*>(&As[buf][kk][64 + ty * 4]);
+      const double2* bp0 = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
+      const double2* bp1 = reinterpret_cast<const double2*>(&Bs[buf][kk][64 + tx * 4]);
+      double2 v;
+      v = ap0[0]; a[0] = v.x; a[1] = v.y;
+      v = ap0[1]; a[2] = v.x; a[3] = v.y;
+      v = ap1[0]; a[4] = v.x; a[5] = v.y;
+      v = ap1[1]; a[6] = v.x; a[7] = v.y;
+      v = bp0[0]; b[0] = v.x; b[1] = v.y;
+      v = bp0[1]; b[2] = v.x; b[3] = v.y;
+      v = bp1[0]; b[4] = v.x; b[5] = v.y;
+      v = bp1[1]; b[6] = v.x; b[7] = v.y;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+    };
+    if (kk_end == kDK) {
+#pragma unroll
+      for (int kk = 0; kk < kDK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kk_end; ++kk) step(kk);
     }
-    __syncthreads();
-    const int kk_end = (int)min((int64_t)kDK, K - k0);
-    for (int kk = 0; kk < kk_end; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
-    }
+    if (kt + 1 < nk) stash(buf ^ 1);
     __syncthreads();
   }
   uint32_t bad = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = m0 + ty * 4 + i;
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t col = n0 + tx * 4 + j;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t col = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
       if (row < M && col < N) {
         const float c = __double2float_rn(acc[i][j]);
         uint32_t v = 0;
