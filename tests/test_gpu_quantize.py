@@ -337,3 +337,52 @@ def test_grouped_equals_sequential(q, fmt_ctor, mode):
     assert spec_a.call_counter == spec_b.call_counter
     for g, w in zip(got, want):
         assert torch.equal(g.view(torch.int32), w.view(torch.int32))
+
+
+# ---- full-size, every element: C2 (2^30) and C3 (2^28) against the oracle ------------
+def _parallel_oracle_compare(oracle, fmt, mode, seed, n, chunk, gen, got_slice):
+    """Compare got_slice(lo, hi) with the oracle over [0, n) in chunks, the
+    oracle chunks in parallel (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(lo):
+        hi = min(n, lo + chunk)
+        x = gen(lo, hi)
+        st, want = oracle.quantize(x, fmt, mode, seed=seed, call=0, index_base=lo)
+        return lo, hi, st, want
+
+    import os
+    with ThreadPoolExecutor(max_workers=max(2, min(16, os.cpu_count() or 2))) as ex:
+        for lo, hi, st, want in ex.map(one, range(0, n, chunk)):
+            assert st == 0
+            assert np.array_equal(bits(got_slice(lo, hi)), bits(want.reshape(-1))), lo
+
+
+def test_c2_full_tensor_every_element(q, oracle):
+    n = 1 << 30
+    x = q.random_uniform((n,), 2, 0, -10.0, 10.0)
+    y = q.quantize_fused_at(x, q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic,
+                                           0x15EED), 0)
+    del x
+    yh = y.cpu().numpy()
+    del y
+    _parallel_oracle_compare(
+        oracle, fixed_fmt(8, 4), STOCHASTIC, 0x15EED, n, 1 << 25,
+        lambda lo, hi: oracle.random_uniform(hi - lo, 2, 0, -10.0, 10.0, index_base=lo),
+        lambda lo, hi: yh[lo:hi])
+
+
+def test_c3_full_tensor_every_element(q, oracle):
+    R, L = 65536, 4096
+    x = q.random_uniform((R, L), 3, 0, -1.0, 1.0)
+    x *= torch.exp2(torch.randint(-20, 21, (R, 1), device="cuda",
+                                  generator=torch.Generator("cuda").manual_seed(1)).float())
+    xh = x.cpu().numpy()
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        y = q.quantize_fused_at(x, q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode(mode),
+                                               0x15EED), 0).cpu().numpy()
+        rows = 1 << 11
+        _parallel_oracle_compare(
+            oracle, block_fmt(8, 0), mode, 0x15EED, R * L, rows * L,
+            lambda lo, hi: xh.reshape(-1)[lo:hi].reshape(-1, L),
+            lambda lo, hi: y.reshape(-1)[lo:hi])
