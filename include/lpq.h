@@ -244,6 +244,29 @@ lpq_status lpq_matmul_q_host(const float* A, const float* B, float* C,
                              const lpq_format* f, int mode, uint64_t seed,
                              uint64_t call, int device);
 
+/* ---- data formats on either side of the path (proj/src/io.cpp) --------- */
+
+/* parse_format (io.cpp:132-181): "float[:E:M]", "fixed[:WL:FL[:symmetric]
+ * [:wrap]]", "block[:WL[:tensor|:dimD]]" (defaults float:5:2, fixed:8:4,
+ * block:8:tensor), validated; LPQ_ERR_FORMAT on any grammar/range error. */
+lpq_status lpq_parse_format(const char* text, lpq_format* out);
+/* parse_rounding (io.cpp:200-206): stochastic | nearest_even | nearest_away |
+ * nearest_zero. */
+lpq_status lpq_parse_rounding(const char* text, int* mode);
+/* format_to_string (io.cpp:183-198); returns the string length. */
+int lpq_format_to_string(const lpq_format* f, char* buf, size_t len);
+/* LPT1 tensor files (io.cpp:54-99): header query, payload load, save. */
+lpq_status lpq_tensor_file_info(const char* path, int64_t* shape /*[8]*/,
+                                int* rank);
+lpq_status lpq_load_tensor_file(const char* path, float* dst, int64_t n);
+lpq_status lpq_save_tensor_file(const char* path, const float* data,
+                                const int64_t* shape, int rank);
+/* `lpsim quantize IN OUT` (proj/tools/lpsim_main.cpp:23-34) on the GPU: LPT1
+ * in -> page-locked memory -> pipelined quantize -> LPT1 out. */
+lpq_status lpq_quantize_file(const char* in_path, const char* out_path,
+                             const lpq_format* f, int mode, uint64_t seed,
+                             uint64_t call, int device);
+
 /* Release the per-device contexts the host entry points created. */
 void lpq_shutdown(void);
 

@@ -18,6 +18,7 @@
 
 #include "lpsim/errors.hpp"
 #include "lpsim/formats.hpp"
+#include "lpsim/io.hpp"
 #include "lpsim/quant_ops.hpp"
 #include "lpsim/rng.hpp"
 #include "lpsim/scalar_quant.hpp"
@@ -201,6 +202,44 @@ int lpsr_quantized_matmul(const float* a, const float* b, float* c, int64_t m,
     lpsim::Tensor tc = lpsim::quantized_matmul(ta, tb, spec);
     *call_counter = spec.call_counter;
     std::memcpy(c, tc.data(), sizeof(float) * static_cast<size_t>(m * n));
+  });
+}
+
+// parse_format (io.cpp:132-181) -> flat format struct
+int lpsr_parse_format(const char* text, RefFormat* out) {
+  return guarded([&] {
+    const auto fmt = lpsim::parse_format(text);
+    RefFormat r{};
+    r.block_dim = -1;
+    if (const auto* f = std::get_if<lpsim::FloatFormat>(&fmt)) {
+      r.kind = 0; r.exp_bits = f->exp_bits; r.man_bits = f->man_bits;
+    } else if (const auto* f = std::get_if<lpsim::FixedFormat>(&fmt)) {
+      r.kind = 1; r.wl = f->wl; r.fl = f->fl; r.symmetric = f->symmetric; r.saturate = f->saturate;
+    } else {
+      const auto& b = std::get<lpsim::BlockFloatFormat>(fmt);
+      r.kind = 2; r.wl = b.wl; r.block_dim = b.block_dim ? *b.block_dim : -1;
+    }
+    *out = r;
+  });
+}
+
+int lpsr_write_tensor_file(const char* path, const float* x, const int64_t* shape, int rank) {
+  return guarded([&] {
+    int64_t n = 1;
+    for (int d = 0; d < rank; ++d) n *= shape[d];
+    lpsim::set_validation(false);
+    lpsim::Tensor t(to_shape(shape, rank), std::vector<float>(x, x + n));
+    lpsim::set_validation(true);
+    lpsim::write_tensor_file(path, t);
+  });
+}
+
+int lpsr_read_tensor_file(const char* path, float* y, int64_t n, int64_t* shape, int* rank) {
+  return guarded([&] {
+    lpsim::Tensor t = lpsim::read_tensor_file(path);
+    *rank = t.rank();
+    for (int d = 0; d < t.rank(); ++d) shape[d] = t.extent(d);
+    if (t.numel() <= n) std::memcpy(y, t.data(), sizeof(float) * static_cast<size_t>(t.numel()));
   });
 }
 

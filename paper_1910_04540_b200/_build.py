@@ -36,7 +36,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 SOURCES = ["capi.cu", "runtime.cu", "elementwise.cu", "block.cu",
            "block_cluster.cu", "gemm.cu", "composed.cu", "optim.cu",
-           "group.cu"]
+           "group.cu", "io.cu"]
 HEADERS = ["quant_math.cuh", "kernels.cuh", "runtime.h", "block_common.cuh"]
 
 NVCC_FLAGS = [

@@ -130,6 +130,14 @@ _PROTOS = {
     "lpq_quantize_grouped": (C.c_int, [C.POINTER(LpqTensorDesc), C.c_int, _F,
                                        C.c_int, C.c_uint64, _VP, C.c_size_t,
                                        _VP, _VP]),
+    "lpq_parse_format": (C.c_int, [C.c_char_p, _F]),
+    "lpq_parse_rounding": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
+    "lpq_format_to_string": (C.c_int, [_F, C.c_char_p, C.c_size_t]),
+    "lpq_tensor_file_info": (C.c_int, [C.c_char_p, _I64P, C.POINTER(C.c_int)]),
+    "lpq_load_tensor_file": (C.c_int, [C.c_char_p, _VP, C.c_int64]),
+    "lpq_save_tensor_file": (C.c_int, [C.c_char_p, _VP, _I64P, C.c_int]),
+    "lpq_quantize_file": (C.c_int, [C.c_char_p, C.c_char_p, _F, C.c_int,
+                                    C.c_uint64, C.c_uint64, C.c_int]),
     "lpq_shutdown": (None, []),
 }
 

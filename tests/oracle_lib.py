@@ -187,11 +187,32 @@ class RefLib:
                                             C.c_uint64,
                                             C.POINTER(C.c_uint64)]
         L.lpsr_set_num_threads.argtypes = [C.c_int]
+        L.lpsr_parse_format.argtypes = [C.c_char_p, C.POINTER(Fmt)]
+        L.lpsr_write_tensor_file.argtypes = [C.c_char_p, _fp, _i64p, C.c_int]
+        L.lpsr_read_tensor_file.argtypes = [C.c_char_p, _fp, C.c_int64, _i64p,
+                                            C.POINTER(C.c_int)]
         L.lpsr_pass_count.restype = C.c_uint64
         self.L = L
 
     def set_num_threads(self, n):
         self.L.lpsr_set_num_threads(n)
+
+    def parse_format(self, text):
+        f = Fmt()
+        st = self.L.lpsr_parse_format(text.encode(), C.byref(f))
+        return st, f
+
+    def write_tensor_file(self, path, x):
+        x = np.asarray(x, dtype=np.float32, order="C")  # keeps rank 0
+        return self.L.lpsr_write_tensor_file(path.encode(), x.reshape(-1),
+                                             np.array(x.shape, np.int64), x.ndim)
+
+    def read_tensor_file(self, path, n):
+        y = np.empty(max(n, 1), np.float32)
+        shape = np.zeros(8, np.int64)
+        rank = C.c_int()
+        st = self.L.lpsr_read_tensor_file(path.encode(), y, n, shape, C.byref(rank))
+        return st, y[:n], tuple(int(v) for v in shape[:rank.value])
 
     def variate(self, seed, call, index):
         return self.L.lpsr_uniform_variate(seed, call, index)

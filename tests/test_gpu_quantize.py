@@ -386,3 +386,29 @@ def test_c3_full_tensor_every_element(q, oracle):
             oracle, block_fmt(8, 0), mode, 0x15EED, R * L, rows * L,
             lambda lo, hi: xh.reshape(-1)[lo:hi].reshape(-1, L),
             lambda lo, hi: y.reshape(-1)[lo:hi])
+
+
+# ---- `lpsim quantize` on the GPU: LPT1 -> quantize -> LPT1 ---------------------------
+@pytest.mark.parametrize("fmt,mode,shape", [
+    (fixed_fmt(8, 4), STOCHASTIC, (3, 1000, 7)), (float_fmt(5, 2), NEAREST_EVEN, (100001,)),
+    (block_fmt(8, 0), STOCHASTIC, (64, 4096)), (block_fmt(8), NEAREST_EVEN, (5, 40001))])
+def test_quantize_file_vs_oracle(q, oracle, tmp_path, fmt, mode, shape):
+    from paper_1910_04540_b200 import io as lio
+    rng = np.random.default_rng(sum(shape))
+    x = (rng.standard_normal(shape) * 3).astype(np.float32)
+    src, dst = str(tmp_path / "in.lpt"), str(tmp_path / "out.lpt")
+    lio.write_tensor_file(src, x)
+    spec = spec_of(q, fmt, mode, seed=0x15EED)
+    spec.call_counter = 4
+    lio.quantize_file(src, dst, spec)
+    got = lio.read_tensor_file(dst)
+    st, want = oracle.quantize(x, fmt, mode, seed=0x15EED, call=4)
+    assert got.shape == x.shape and np.array_equal(bits(got), bits(want))
+    assert spec.call_counter == (5 if mode == STOCHASTIC else 4)
+    bad = x.copy()
+    bad.reshape(-1)[3] = np.inf
+    lio.write_tensor_file(src, bad)
+    with pytest.raises(q.InvalidInputError):
+        lio.quantize_file(src, dst, spec)
+    with pytest.raises(q.FormatError):
+        lio.quantize_file(str(tmp_path / "missing.lpt"), dst, spec)
