@@ -6,7 +6,8 @@
 // b along `extent` (formats.hpp:69-78).  Three plans:
 //
 //  * kRowsInRegisters (outer == 1, contiguous block <= 32768 floats, aligned):
-//    ONE HBM pass.  One CTA per block ("row"): the row is loaded into
+//    ONE HBM pass.  Rows <= 512 floats: a group of <= 32 lanes per row, several
+//    rows per warp.  Longer rows: one CTA per block ("row"): the row is loaded into
 //    registers with 128-bit loads, max-reduced with warp REDUX + shared
 //    memory, the shared exponent derived in registers, the row quantized and
 //    stored.  8 algorithmic bytes per element.  (BASELINE config C3.)
@@ -96,6 +97,69 @@ __global__ void __launch_bounds__(T)
   if (lane == 0) flag(status, bad);
 }
 
+// Short rows (L <= 512 floats): G lanes per row (G a power of two <= 32),
+// V float4 per lane, 32/G rows per warp, 8 warps per CTA; the row maximum is
+// a butterfly over the row's G lanes.  (One CTA per 64-float row would leave
+// most of each CTA idle and make the launch CTA-rate-bound.)
+template <int M, int G, int V, bool IDX4>
+__global__ void __launch_bounds__(256)
+    k_block_rows_small(const float* __restrict__ x, float* __restrict__ y,
+                       int64_t L, int64_t nrows, uint64_t base, uint64_t key,
+                       int wl, RngMul m32, uint32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = ((int64_t)blockIdx.x * 8 + warp) * (32 / G) + lane / G;
+  const int g = lane % G;
+  const int64_t L4 = L >> 2;
+  const bool live = r < nrows;
+  const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
+  float4 v[V];
+  float mf = 0.0f, nf = 0.0f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int64_t j = g + (int64_t)k * G;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live && j < L4) {
+      v[k] = __ldcs(xr + j);
+      absmax_nf(v[k], mf, nf);
+    }
+  }
+  uint32_t m = f2u(mf);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  const BlockScale sc = make_block_scale(m, wl);
+  const float kmin = -(float)(1 << (wl - 1));
+  const float kmax = (float)((1 << (wl - 1)) - 1);
+  if (live) {
+    float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
+    const uint64_t row_base = base + (uint64_t)(r * L);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int64_t j = g + (int64_t)k * G;
+      if (j < L4)
+        __stcs(yr + j, two_factor(sc)
+                           ? qb4<M, true, IDX4>(v[k], sc, kmin, kmax, key, row_base + 4 * j, m32)
+                           : qb4<M, false, IDX4>(v[k], sc, kmin, kmax, key, row_base + 4 * j, m32));
+    }
+  }
+  uint32_t bad = live ? ((sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u)) : 0u;
+  bad = __reduce_or_sync(kFull, bad);
+  if (lane == 0) flag(status, bad);
+}
+
+template <int M, int G, int V>
+void launch_rows_small_t(const float* x, float* y, int64_t L, int64_t nrows,
+                         uint64_t base, uint64_t key, int wl, uint32_t* st,
+                         cudaStream_t s) {
+  const int64_t per_cta = 8 * (32 / G);
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((nrows + per_cta - 1) / per_cta, 0x7FFFFFFF));
+  if ((base & 3u) == 0)
+    k_block_rows_small<M, G, V, true><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+  else
+    k_block_rows_small<M, G, V, false><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+  note_launch();
+}
+
 template <int M, int T, int VPT>
 void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
                    uint64_t base, uint64_t key, int wl, uint32_t* st,
@@ -114,7 +178,14 @@ void launch_rows(const float* x, float* y, int64_t L, int64_t nrows,
                  uint64_t base, uint64_t key, int wl, uint32_t* st,
                  cudaStream_t s) {
   const int64_t L4 = L >> 2;
-  if (L4 <= 128) launch_rows_t<M, 128, 1>(x, y, L, nrows, base, key, wl, st, s);
+  if (L4 <= 1) launch_rows_small_t<M, 1, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 2) launch_rows_small_t<M, 2, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 4) launch_rows_small_t<M, 4, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 8) launch_rows_small_t<M, 8, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 16) launch_rows_small_t<M, 16, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 32) launch_rows_small_t<M, 32, 1>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 64) launch_rows_small_t<M, 32, 2>(x, y, L, nrows, base, key, wl, st, s);
+  else if (L4 <= 128) launch_rows_small_t<M, 32, 4>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 256) launch_rows_t<M, 256, 1>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 512) launch_rows_t<M, 256, 2>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 1024) launch_rows_t<M, 128, 8>(x, y, L, nrows, base, key, wl, st, s);
@@ -415,10 +486,20 @@ cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
   return cudaGetLastError();
 }
 
+bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y) {
+  return g.outer == 1 && g.stride % 4 == 0 && aligned16(x) && aligned16(y) &&
+         g.stride > 32768 && g.stride <= (int64_t(1) << 20);
+}
+
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
   const bool rows = g.outer == 1 && g.stride % 4 == 0 && aligned16(x) && aligned16(y);
-  if (rows && g.stride <= 32768 && g.stride >= 64) return BlockPlan::kRowsInRegisters;
-  if (rows && g.stride > 32768 && cluster_size_for(g.stride) > 0)
+  if (rows && g.stride <= 32768 && g.stride >= 4) return BlockPlan::kRowsInRegisters;
+  // cluster plan: rows of at most 1M floats (L2-resident second read) and
+  // enough (row, CTA) pairs to fill the SMs; a few huge rows stream through
+  // every SM with the two-pass segment plan instead (quantize_device still
+  // takes the cluster plan when the caller supplied no workspace)
+  if (block_cluster_ok(g, x, y) &&
+      g.extent * cluster_size_for(g.stride) >= 2 * (int64_t)device_info().sm_count)
     return BlockPlan::kRowsCluster;
   if (g.stride >= 1024) return BlockPlan::kTwoPassSegments;
   return BlockPlan::kTwoPassColumns;

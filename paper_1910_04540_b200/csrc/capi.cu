@@ -147,9 +147,12 @@ lpq_status quantize_device(const float* x, float* y, const int64_t* shape,
     e = launch_float(x, y, n, index_base, key, p, mode, d_status, s);
     note_passes(1);
   } else {
-    const BlockPlan plan = block_plan(g, x, y);
+    BlockPlan plan = block_plan(g, x, y);
     const size_t need = block_workspace(g, plan);
-    if (need > 0 && (!ws || ws_bytes < need)) return LPQ_ERR_WORKSPACE;
+    if (need > 0 && (!ws || ws_bytes < need)) {
+      if (!block_cluster_ok(g, x, y)) return LPQ_ERR_WORKSPACE;
+      plan = BlockPlan::kRowsCluster;  // single pass, no workspace
+    }
     e = launch_block(x, y, g, plan, index_base, key, f->wl, mode, ws, d_status, s);
     note_passes(block_plan_passes(plan));
   }

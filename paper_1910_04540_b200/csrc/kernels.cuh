@@ -43,6 +43,8 @@ struct BlockGeom {
 enum class BlockPlan { kRowsInRegisters, kRowsCluster, kTwoPassSegments,
                        kTwoPassColumns };
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y);
+// the cluster (single-pass) plan can run this geometry
+bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y);
 inline int block_plan_passes(BlockPlan p) {
   return (p == BlockPlan::kRowsInRegisters || p == BlockPlan::kRowsCluster) ? 1 : 2;
 }

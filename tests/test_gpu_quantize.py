@@ -137,10 +137,15 @@ BLOCK_CASES = [
     ((300, 4096), 0),       # rows in registers, 1024x4
     ((64, 100), 0),         # rows, 128 threads
     ((7, 20000), 0),        # rows, 1024 x 8 float4
-    ((5, 40000), 0),        # long rows -> cluster plan (1 CTA per row)
-    ((3, 200000), 0),       # cluster plan, 4 CTAs per row, DSMEM max exchange
-    ((2, 802816), 0),       # ResNet-50 conv1 per-sample block, 15-CTA cluster
-    ((1, 3, 99996), 1),     # cluster plan along dim 1 (leading 1)
+    ((5, 40000), 0),        # few long rows -> two-pass segments
+    ((300, 40000), 0),      # cluster plan (1 CTA per row)
+    ((80, 200000), 0),      # cluster plan, 4 CTAs per row, DSMEM max exchange
+    ((24, 802816), 0),      # ResNet-50 conv1 per-sample block, 13-CTA clusters
+    ((1, 300, 40000), 1),   # cluster plan along dim 1 (leading 1)
+    ((4096, 64), 0),        # short rows: 16 lanes per row
+    ((999, 12), 0),         # short rows: 4 lanes per row
+    ((77, 400), 0),         # short rows: 32 lanes x 4 float4
+    ((33, 4), 0),           # short rows: 1 lane per row
     ((2, 3, 99_999), 2),    # last dim of odd length -> two-pass columns
     ((1000,), None),        # whole tensor, rows plan (1 row)
     ((1_000_003,), None),   # whole tensor, two-pass segments, odd length
@@ -231,7 +236,8 @@ def test_pass_count_contract(q):
     rng = np.random.default_rng(71)
     cases = [(q.FixedFormat(8, 4), (32, 32), 1), (q.FloatFormat(5, 2), (32, 32), 1),
              (q.BlockFloatFormat(8, 0), (16, 256), 1), (q.BlockFloatFormat(8), (32, 32), 1),
-             (q.BlockFloatFormat(8), (8, 40000), 1), (q.BlockFloatFormat(8), (3, 999_999), 2),
+             (q.BlockFloatFormat(8), (8, 40000), 2), (q.BlockFloatFormat(8, 0), (300, 40000), 1),
+             (q.BlockFloatFormat(8), (3, 999_999), 2),
              (q.BlockFloatFormat(8, 1), (32, 32), 2)]
     for fmt, shape, passes in cases:
         t = dev(rng.uniform(-4, 4, shape).astype(np.float32))
