@@ -223,6 +223,43 @@ int lpsr_parse_format(const char* text, RefFormat* out) {
   });
 }
 
+// parse_quant_config (io.cpp:294-321) -> five (present, format, mode, seed)
+// slots in the category order weight, accumulator, gradient, activation,
+// error.  nlohmann type errors (json::exception other than the parse error the
+// reference converts) return 7.
+int lpsr_parse_quant_config(const char* text, uint64_t default_seed,
+                            int32_t* present, RefFormat* fmts, int32_t* modes,
+                            uint64_t* seeds) {
+  try {
+    const lpsim::QuantConfig cfg = lpsim::parse_quant_config(text, default_seed);
+    const std::optional<lpsim::QuantSpec>* slots[5] = {
+        &cfg.weight, &cfg.accumulator, &cfg.gradient, &cfg.activation, &cfg.error};
+    for (int i = 0; i < 5; ++i) {
+      present[i] = slots[i]->has_value();
+      if (!present[i]) continue;
+      const auto& sp = **slots[i];
+      RefFormat r{};
+      r.block_dim = -1;
+      if (const auto* f = std::get_if<lpsim::FloatFormat>(&sp.format)) {
+        r.kind = 0; r.exp_bits = f->exp_bits; r.man_bits = f->man_bits;
+      } else if (const auto* f = std::get_if<lpsim::FixedFormat>(&sp.format)) {
+        r.kind = 1; r.wl = f->wl; r.fl = f->fl; r.symmetric = f->symmetric; r.saturate = f->saturate;
+      } else {
+        const auto& b = std::get<lpsim::BlockFloatFormat>(sp.format);
+        r.kind = 2; r.wl = b.wl; r.block_dim = b.block_dim ? *b.block_dim : -1;
+      }
+      fmts[i] = r;
+      modes[i] = static_cast<int32_t>(sp.mode);
+      seeds[i] = sp.seed;
+    }
+    return 0;
+  } catch (const lpsim::format_error&) {
+    return 1;
+  } catch (const std::exception&) {
+    return 7;
+  }
+}
+
 int lpsr_write_tensor_file(const char* path, const float* x, const int64_t* shape, int rank) {
   return guarded([&] {
     int64_t n = 1;

@@ -57,6 +57,14 @@ class LowPrecisionOptimizer:
         self.acc = [p.detach().clone().contiguous() for p in self.params]
         self.vel = [torch.zeros_like(p) for p in self.params]
 
+    @classmethod
+    def from_config(cls, params: Sequence, lr: float, momentum: float, cfg):
+        """LowPrecisionOptimizer(model, lr, momentum, cfg) with a QuantConfig
+        (io.parse_quant_config); uses its weight/accumulator/gradient specs
+        (train.cpp:130-146)."""
+        return cls(params, lr, momentum, weight=cfg.weight,
+                   accumulator=cfg.accumulator, gradient=cfg.gradient)
+
     def accumulators(self):
         return self.acc
 

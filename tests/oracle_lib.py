@@ -191,6 +191,10 @@ class RefLib:
         L.lpsr_write_tensor_file.argtypes = [C.c_char_p, _fp, _i64p, C.c_int]
         L.lpsr_read_tensor_file.argtypes = [C.c_char_p, _fp, C.c_int64, _i64p,
                                             C.POINTER(C.c_int)]
+        L.lpsr_parse_quant_config.argtypes = [
+            C.c_char_p, C.c_uint64, np.ctypeslib.ndpointer(np.int32, flags="C"),
+            C.POINTER(Fmt), np.ctypeslib.ndpointer(np.int32, flags="C"),
+            np.ctypeslib.ndpointer(np.uint64, flags="C")]
         L.lpsr_pass_count.restype = C.c_uint64
         self.L = L
 
@@ -201,6 +205,18 @@ class RefLib:
         f = Fmt()
         st = self.L.lpsr_parse_format(text.encode(), C.byref(f))
         return st, f
+
+    def parse_quant_config(self, text, default_seed):
+        """-> (status, [None | (Fmt, mode, seed)] x 5)"""
+        present = np.zeros(5, np.int32)
+        fmts = (Fmt * 5)()
+        modes = np.zeros(5, np.int32)
+        seeds = np.zeros(5, np.uint64)
+        st = self.L.lpsr_parse_quant_config(text.encode(), C.c_uint64(default_seed),
+                                            present, fmts, modes, seeds)
+        out = [(fmts[i], int(modes[i]), int(seeds[i])) if present[i] else None
+               for i in range(5)]
+        return st, out
 
     def write_tensor_file(self, path, x):
         x = np.asarray(x, dtype=np.float32, order="C")  # keeps rank 0

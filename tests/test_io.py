@@ -77,3 +77,83 @@ def test_lpt1_errors(tmp_path):
         lio.read_tensor_file(str(tmp_path / "missing.lpt"))
     with pytest.raises(ValueError):
         lio.write_tensor_file(p, np.ones((1,) * 9, np.float32))
+
+
+# ---------------------------------------------------------------------------
+# JSON quantization config (io.cpp:208-329) against the reference parser, with
+# the cases of proj/tests/test_io.cpp plus type/edge cases
+CONFIGS = [
+    '{}',
+    '{"weight": {"kind": "float", "exp": 5, "man": 2}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "rounding": "stochastic", "seed": 9}}',
+    '{"gradient": {"kind": "fixed", "wl": 8, "fl": 4, "symmetric": true, "saturate": false}}',
+    '{"activation": {"kind": "block", "wl": 8, "block": "tensor"}, "error": {"kind": "block", "wl": 6, "block": {"dim": 1}}}',
+    '{"accumulator": {"kind": "float", "exp": 8, "man": 23, "rounding": "nearest_zero"}}',
+    '{"weight": {"kind": "block", "wl": 8}, "accumulator": {"kind": "fixed", "wl": 16, "fl": 8},'
+    ' "gradient": {"kind": "float", "exp": 5, "man": 2, "rounding": "nearest_away"},'
+    ' "activation": {"kind": "fixed", "wl": 8, "fl": 4}, "error": {"kind": "float", "exp": 4, "man": 3}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "seed": 18446744073709551615}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "seed": -1}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "seed": 3.75}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "seed": true}}',
+    '{"weight": {"kind": "fixed", "wl": 4294967304, "fl": 4}}',      # wraps to 8
+    '{"weight": {"kind": "float", "exp": 5, "man": 2}, "weight": {"kind": "fixed", "wl": 8, "fl": 4}}',
+    # rejected
+    '[]', '3', 'not json', '{"weight": 3}', '{"bias": {"kind": "float", "exp": 5, "man": 2}}',
+    '{"weight": {"exp": 5, "man": 2}}', '{"weight": {"kind": "decimal"}}',
+    '{"weight": {"kind": "float", "exp": 5}}', '{"weight": {"kind": "float", "exp": 5.0, "man": 2}}',
+    '{"weight": {"kind": "float", "exp": 9, "man": 2}}',
+    '{"weight": {"kind": "float", "exp": 5, "man": 2, "wl": 8}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "block": "tensor"}}',
+    '{"weight": {"kind": "block", "wl": 8, "fl": 1}}',
+    '{"weight": {"kind": "block", "wl": 8, "block": {"dim": -1}}}',
+    '{"weight": {"kind": "block", "wl": 8, "block": {"dim": 1, "x": 2}}}',
+    '{"weight": {"kind": "block", "wl": 8, "block": "rows"}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "rounding": "up"}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "colour": 1}}',
+    '{"weight": {"kind": "float", "exp": NaN, "man": 2}}',
+    # type errors (the reference's json library throws type_error)
+    '{"weight": {"kind": 3}}', '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "symmetric": 1}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "seed": "7"}}',
+    '{"weight": {"kind": "fixed", "wl": 8, "fl": 4, "rounding": 0}}',
+]
+
+
+@pytest.mark.parametrize("text", CONFIGS)
+@pytest.mark.parametrize("default_seed", [0, 0x15EED, 2**64 - 1])
+def test_quant_config_matches_reference(ref, text, default_seed):
+    from paper_1910_04540_b200 import io as lio
+    from paper_1910_04540_b200._lib import FormatError
+    st, want = ref.parse_quant_config(text, default_seed)
+    if st == 1:
+        with pytest.raises(FormatError):
+            lio.parse_quant_config(text, default_seed)
+        return
+    if st == 7:
+        with pytest.raises(lio.ConfigTypeError):
+            lio.parse_quant_config(text, default_seed)
+        return
+    assert st == 0
+    cfg = lio.parse_quant_config(text, default_seed)
+    for name, w in zip(("weight", "accumulator", "gradient", "activation", "error"), want):
+        got = getattr(cfg, name)
+        if w is None:
+            assert got is None, name
+            continue
+        wf, wmode, wseed = w
+        f = got.format.c()
+        for field, _ in f._fields_:
+            assert getattr(f, field) == getattr(wf, field), (text, name, field)
+        assert int(got.mode) == wmode and got.seed == wseed and got.call_counter == 0
+
+
+def test_load_quant_config(tmp_path):
+    from paper_1910_04540_b200 import io as lio
+    from paper_1910_04540_b200._lib import FormatError
+    p = tmp_path / "cfg.json"
+    p.write_text('{"gradient": {"kind": "fixed", "wl": 8, "fl": 4, "rounding": "stochastic"}}')
+    cfg = lio.load_quant_config(str(p), 5)
+    assert cfg.weight is None and cfg.gradient.format.wl == 8
+    assert cfg.gradient.seed == lio._mix64(5 ^ lio._mix64(2))
+    with pytest.raises(FormatError):
+        lio.load_quant_config(str(tmp_path / "missing.json"), 5)
