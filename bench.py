@@ -327,10 +327,32 @@ def run_ours(args, rank, world, local_rank):
             et = float(t.item())
         # the host result must equal the device result
         assert torch.equal(hy.view(torch.int32), ys[0].cpu().view(torch.int32))
+        # the PCIe ceiling for the same bytes: a bare H2D of the input concurrent
+        # with a bare D2H of the output (two streams, same host buffers), no
+        # kernel -- what the e2e number is bounded by
+        ceiling = None
+        if host_mem == "pinned":
+            dtmp = torch.empty_like(xs[0])
+            s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            ct = []
+            for _ in range(3):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                with torch.cuda.stream(s_in):
+                    dtmp.copy_(hx, non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    hy.copy_(ys[0], non_blocking=True)
+                torch.cuda.synchronize(dev)
+                ct.append(time.perf_counter() - t0)
+            ceiling = round(bytes_per_rank_step / min(ct) / 1e9, 3)
+            del dtmp
         e2e = {"value": round(bytes_per_rank_step * world * e_steps / et / 1e9, 3),
                "unit": "GB/s", "h2d_bytes_per_step": 4 * n * world,
                "d2h_bytes_per_step": 4 * n * world, "steps": e_steps,
-               "api": f"lpq_quantize_host (include/lpq.h), {host_mem} host buffers"}
+               "api": f"lpq_quantize_host (include/lpq.h), {host_mem} host buffers",
+               "pcie_copy_ceiling": ceiling,
+               "pcie_copy_ceiling_note": "per GPU: concurrent bare H2D(input)+D2H(output) copies "
+                                         "of the same pinned buffers, metric units"}
         del hx, hy
     # ---- roofline of the dominant kernel --------------------------------------------
     peak, peak_src, peaks = load_peaks()

@@ -28,7 +28,7 @@ __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
   if (M == kStochastic) v = variate24_zb(z, rm.m32);
   if (M == kNearestEven || M == kStochastic)
     return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
-        x, s, kmin, kmax, v);
+        x, s, kmin, kmax, v, rm.m2, rm.neg1);
   return quant_block<M>(x, s, kmin, kmax, v);
 }
 

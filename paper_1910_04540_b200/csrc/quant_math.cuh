@@ -195,9 +195,11 @@ struct RngMul {
   uint32_t m4;    // 4      (>> 30 as hi(x * 4))
   uint32_t m32;   // 32     (>> 27 as hi(x * 32))
   uint32_t m24;   // 2^24   (>> 8  as hi(x * 2^24))
+  uint32_t m2;    // 2      (>> 31 as hi(x * 2))
+  uint32_t neg1;  // 2^32-1 (-x as x * neg1)
 };
 
-LPQ_HD RngMul rng_mul() { return RngMul{1u, 4u, 32u, 1u << 24}; }
+LPQ_HD RngMul rng_mul() { return RngMul{1u, 4u, 32u, 1u << 24, 2u, 0xFFFFFFFFu}; }
 
 LPQ_HD uint64_t mad_wide_u32(uint32_t a, uint32_t b, uint64_t c) {
 #if defined(__CUDA_ARCH__)
@@ -574,20 +576,31 @@ LPQ_HD float quant_block(float x, const BlockScale& s, float kmin, float kmax,
 // Block element, streaming form for NearestEven / Stochastic: signed
 // rounding (round_signed), k * delta + 0 in one FFMA (-0 -> +0, and a single
 // rounding of the exact k * 2^shift).  TWO: the scales needed two factors
-// (block maxima near the fp32 range ends).  A product x * 2^-shift that
-// flushed to zero is replaced by the smallest denormal with x's sign, which
-// gives the exact stochastic decision (u < |r| iff u == 0 for r > 0; never
-// for r < 0).  All-zero blocks have zero scales and produce +0.  Identical
-// results to quant_block<M>.
+// (block maxima near the fp32 range ends).  All-zero blocks have zero scales
+// and produce +0.  Identical results to quant_block<M>.
+//  * No lower clamp: |x| <= max < 2^(E+1), so |r| < 2^(wl-1) and every
+//    rounding of r is >= -2^(wl-1) = kmin; only k = 2^(wl-1) needs clamping.
+//  * Stochastic: a positive x whose r flushed to +0 takes the smallest
+//    denormal, which gives the exact decision (k = 1 iff u == 0).  A negative
+//    flushed r gives k = 0 for every u, as the exact r would.  The guard is
+//    r_bits = max(r_bits, t) with t = (-x_bits) >> 31 (1 for x > +0, and for
+//    x = -0 whose r_bits 0x80000000 it leaves unchanged), formed with IMADs
+//    against runtime multipliers (neg1 = 2^32-1, m2 = 2) so it issues on the
+//    FMA pipe; one integer max on the ALU pipe.
 template <int M, bool TWO>
 LPQ_HD float quant_block_fast(float x, const BlockScale& s, float kmin,
-                              float kmax, uint32_t v) {
+                              float kmax, uint32_t v, uint32_t m2 = 2u,
+                              uint32_t neg1 = 0xFFFFFFFFu) {
+  (void)kmin;
   float r = fmul(x, s.s1);
   if (TWO) r = fmul(r, s.s2);
-  if (M == kStochastic && r == 0.0f && x != 0.0f)
-    r = x < 0.0f ? -0x1p-149f : 0x1p-149f;
+  if (M == kStochastic) {
+    const uint32_t t = umulhi32(f2u(x) * neg1, m2);
+    const uint32_t rb = f2u(r);
+    r = u2f(rb > t ? rb : t);
+  }
   float k = round_signed<M>(r, v);
-  k = fminf(fmaxf(k, kmin), kmax);
+  k = fminf(k, kmax);
   if (TWO) return fma_rn(fmul(k, s.o1), s.o2, 0.0f);
   return fma_rn(k, s.o1, 0.0f);
 }
