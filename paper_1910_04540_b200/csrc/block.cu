@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "block_common.cuh"
 #include "kernels.cuh"
@@ -35,19 +36,39 @@ using namespace blk;
 // ---------------------------------------------------------------------------
 // Plan 1: one row per CTA, held in registers (single HBM pass).
 // T threads, VPT float4 per thread; row length L (multiple of 4, <= 4*T*VPT).
-template <int M, int T, int VPT, bool IDX4>
+// FULL: L == 4*T*VPT (no bounds tests).  The row maximum propagates NaN
+// (absmax_nan); a NaN row recomputes the NaN-ignoring maximum of
+// reduce_max_abs and flags the non-finite input.  Three element loops per
+// block class: two-factor scales, single factor with the stochastic flush
+// guard (s1 < 1), single factor without.
+template <int T>
+__device__ __forceinline__ uint32_t cta_max(uint32_t m, uint32_t* red,
+                                            uint32_t* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  m = __reduce_max_sync(kFull, m);  // non-negative floats: uint order
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < T / 32 ? red[lane] : 0u;
+    t = __reduce_max_sync(kFull, t);
+    if (lane == 0) *out = t;
+  }
+  __syncthreads();
+  return *out;
+}
+
+template <int M, int T, int VPT, bool IDX4, bool FULL>
 __global__ void __launch_bounds__(T)
     k_block_rows(const float* __restrict__ x, float* __restrict__ y, int64_t L,
                  int64_t nrows, uint64_t base, uint64_t key, int wl,
                  RngMul m32, uint32_t* __restrict__ status) {
   __shared__ uint32_t red[T / 32];
   __shared__ uint32_t row_max;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
   const int64_t L4 = L >> 2;
   uint32_t bad = 0;
-  float nf = 0.0f;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
     float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
@@ -56,43 +77,43 @@ __global__ void __launch_bounds__(T)
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int64_t j = threadIdx.x + (int64_t)k * T;
-      if (j < L4) {
+      if (FULL || j < L4) {
         v[k] = __ldcs(xr + j);
-        absmax_nf(v[k], mf, nf);
+        absmax_nan(v[k], mf);
       }
     }
-    uint32_t m = __reduce_max_sync(kFull, f2u(mf));  // non-negative: uint order
-    if (lane == 0) red[warp] = m;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t t = lane < T / 32 ? red[lane] : 0u;
-      t = __reduce_max_sync(kFull, t);
-      if (lane == 0) row_max = t;
+    uint32_t m = cta_max<T>(f2u(mf), red, &row_max);
+    if (m > 0x7F800000u) {  // NaN in the row (uniform): slow path
+      bad |= 1u;
+      float nf = 0.0f;
+      mf = 0.0f;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const int64_t j = threadIdx.x + (int64_t)k * T;
+        if (FULL || j < L4) absmax_nf(v[k], mf, nf);
+      }
+      __syncthreads();  // row_max is rewritten
+      m = cta_max<T>(f2u(mf), red, &row_max);
     }
-    __syncthreads();
-    const BlockScale sc = make_block_scale(row_max, wl);
+    const BlockScale sc = make_block_scale(m, wl);
     if (sc.bad) bad |= 2u;
     const uint64_t row_base = base + (uint64_t)(r * L);
-    if (!two_factor(sc)) {
+    auto run = [&](auto two_t, auto guard_t) {
+      constexpr bool TWO = decltype(two_t)::value;
+      constexpr bool GUARD = decltype(guard_t)::value;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
         const int64_t j = threadIdx.x + (int64_t)k * T;
-        if (j < L4)
-          __stcs(yr + j, qb4<M, false, IDX4>(v[k], sc, kmin, kmax, key,
-                                             row_base + 4 * j, m32));
+        if (FULL || j < L4)
+          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(v[k], sc, kmin, kmax, key,
+                                                  row_base + 4 * j, m32));
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        const int64_t j = threadIdx.x + (int64_t)k * T;
-        if (j < L4)
-          __stcs(yr + j, qb4<M, true, IDX4>(v[k], sc, kmin, kmax, key,
-                                            row_base + 4 * j, m32));
-      }
-    }
+    };
+    if (two_factor(sc)) run(std::true_type{}, std::false_type{});
+    else if (M == kStochastic && needs_guard(sc)) run(std::false_type{}, std::true_type{});
+    else run(std::false_type{}, std::false_type{});
     __syncthreads();  // red/row_max are reused by the next row
   }
-  if (nf != nf) bad |= 1u;
   bad = __reduce_or_sync(kFull, bad);
   if (lane == 0) flag(status, bad);
 }
@@ -166,10 +187,13 @@ void launch_rows_t(const float* x, float* y, int64_t L, int64_t nrows,
                    cudaStream_t s) {
   // one CTA per row, all rows launched (CTAs retire in address order)
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, 0x7FFFFFFF));
-  if ((base & 3u) == 0)
-    k_block_rows<M, T, VPT, true><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+  const bool full = (L >> 2) == (int64_t)T * VPT;
+  if ((base & 3u) == 0 && full)
+    k_block_rows<M, T, VPT, true, true><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+  else if ((base & 3u) == 0)
+    k_block_rows<M, T, VPT, true, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   else
-    k_block_rows<M, T, VPT, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+    k_block_rows<M, T, VPT, false, false><<<grid, T, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   note_launch();
 }
 

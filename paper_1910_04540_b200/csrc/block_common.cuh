@@ -21,29 +21,47 @@ __device__ __forceinline__ uint32_t nf4(const float4& v) {
 // TWO: the block's scales need two factors (maxima near the fp32 range
 // ends); uniform per block, so kernels branch once per block/row.
 // z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
-template <int M, bool TWO>
+// GUARD: see quant_block_fast (stochastic flush guard; needs_guard()).
+template <int M, bool TWO, bool GUARD = true>
 __device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
                                     float kmax, uint64_t z, const RngMul& rm) {
   uint32_t v = 0;
   if (M == kStochastic) v = variate24_zb(z, rm.m32);
   if (M == kNearestEven || M == kStochastic)
-    return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO>(
-        x, s, kmin, kmax, v, rm.m2, rm.neg1);
+    return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO,
+                            GUARD>(x, s, kmin, kmax, v, rm.m2, rm.neg1);
   return quant_block<M>(x, s, kmin, kmax, v);
 }
 
 // IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q
-template <int M, bool TWO, bool IDX4>
+template <int M, bool TWO, bool IDX4, bool GUARD = true>
 __device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
                                       float kmin, float kmax, uint64_t key,
                                       uint64_t idx, const RngMul& m32) {
   const uint64_t z0 = key ^ idx;
   float4 o;
-  o.x = qb<M, TWO>(x.x, s, kmin, kmax, z0, m32);
-  o.y = qb<M, TWO>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
-  o.z = qb<M, TWO>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);
-  o.w = qb<M, TWO>(x.w, s, kmin, kmax, IDX4 ? z0 ^ 3u : key ^ (idx + 3), m32);
+  o.x = qb<M, TWO, GUARD>(x.x, s, kmin, kmax, z0, m32);
+  o.y = qb<M, TWO, GUARD>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
+  o.z = qb<M, TWO, GUARD>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);
+  o.w = qb<M, TWO, GUARD>(x.w, s, kmin, kmax, IDX4 ? z0 ^ 3u : key ^ (idx + 3), m32);
   return o;
+}
+
+// single-factor scales with s1 < 1: a product x * s1 can flush to zero
+__device__ __forceinline__ bool needs_guard(const BlockScale& s) {
+  return s.s1 < 1.0f;
+}
+
+// |x| maximum that PROPAGATES NaN (FMNMX3.NAN, 0.5 instructions per
+// element); a NaN row maximum sends the row down absmax_nf's slow path.
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ void absmax_nan(const float4& v, float& m) {
+  m = fmax3_nan(m, fabsf(v.x), fabsf(v.y));
+  m = fmax3_nan(m, fabsf(v.z), fabsf(v.w));
 }
 
 // |x| maximum with NaN ignored (fmaxf returns the non-NaN operand, like

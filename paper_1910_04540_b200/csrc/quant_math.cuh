@@ -587,14 +587,16 @@ LPQ_HD float quant_block(float x, const BlockScale& s, float kmin, float kmax,
 //    x = -0 whose r_bits 0x80000000 it leaves unchanged), formed with IMADs
 //    against runtime multipliers (neg1 = 2^32-1, m2 = 2) so it issues on the
 //    FMA pipe; one integer max on the ALU pipe.
-template <int M, bool TWO>
+//  * GUARD = false skips the guard for blocks with s1 >= 1 (no product can
+//    flush: |r| >= |x| >= 2^-149), and for two-factor scales (s1 = 2^127).
+template <int M, bool TWO, bool GUARD = true>
 LPQ_HD float quant_block_fast(float x, const BlockScale& s, float kmin,
                               float kmax, uint32_t v, uint32_t m2 = 2u,
                               uint32_t neg1 = 0xFFFFFFFFu) {
   (void)kmin;
   float r = fmul(x, s.s1);
   if (TWO) r = fmul(r, s.s2);
-  if (M == kStochastic) {
+  if (M == kStochastic && GUARD) {
     const uint32_t t = umulhi32(f2u(x) * neg1, m2);
     const uint32_t rb = f2u(r);
     r = u2f(rb > t ? rb : t);

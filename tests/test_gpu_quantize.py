@@ -418,3 +418,32 @@ def test_quantize_file_vs_oracle(q, oracle, tmp_path, fmt, mode, shape):
         lio.quantize_file(src, dst, spec)
     with pytest.raises(q.FormatError):
         lio.quantize_file(str(tmp_path / "missing.lpt"), dst, spec)
+
+
+NONFINITE_CASES = [((300, 4096), 0), ((77, 400), 0), ((7, 20000), 0), ((300, 40000), 0),
+                   ((5, 40000), 0), ((50, 70, 30), 1), ((1_000_003,), None), ((4096, 64), 0)]
+
+
+@pytest.mark.parametrize("shape,dim", NONFINITE_CASES)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_block_nonfinite_every_plan(q, shape, dim, mode):
+    # fused_block (quant_ops.cpp:68-115): the block maxima and their range
+    # check (scalar_quant.hpp:72-77) come before the element pass, so a block
+    # holding inf (or >= 2^127) reports the range error even when another
+    # element is NaN; NaN alone (ignored by reduce_max_abs) is the non-finite
+    # input error of quant_pass (quant_ops.cpp:28-29)
+    rng = np.random.default_rng(hash((shape, dim, mode)) % 2**32)
+    x = rng.uniform(-1, 1, shape).astype(np.float32)
+    n = x.size
+    spec = q.QuantSpec(q.BlockFloatFormat(8, dim), q.RoundingMode(mode), 3, 0)
+    i, j = (int(v) for v in rng.choice(n, 2, replace=False))
+    for vals, msg in (({i: np.nan}, "non-finite"), ({i: np.inf}, "too large"),
+                      ({i: -np.inf}, "too large"), ({i: np.nan, j: 2.0**127}, "too large"),
+                      ({i: np.nan, j: -np.nan}, "non-finite")):
+        xb = x.copy().reshape(-1)
+        for k, v in vals.items():
+            xb[k] = v
+        with pytest.raises(q.InvalidInputError, match=msg):
+            q.quantize_fused(dev(xb.reshape(shape)), spec)
+    got = q.quantize_fused_at(dev(x), spec, 0)  # status cleared
+    assert np.isfinite(got.cpu().numpy()).all()
