@@ -407,6 +407,8 @@ struct FloatParams {
   int32_t sc_base;   // 254 + man
   int32_t scaled_ok; // 2 <= exp_bits <= 7
   uint32_t m_sh9;    // 2^9   (runtime multipliers, see RngMul)
+  uint32_t m_two;    // 2
+  uint32_t m_sh8;    // 2^8
   uint32_t m_neg23;  // -2^23 (mod 2^32)
   uint32_t m_pos23;  // 2^23
   uint32_t sc_bits;  // (254 + man) << 23
@@ -434,6 +436,8 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.sc_base = 254 + man_bits;
   p.scaled_ok = (exp_bits >= 2 && exp_bits <= 7) ? 1 : 0;
   p.m_sh9 = 1u << 9;
+  p.m_two = 2u;
+  p.m_sh8 = 1u << 8;
   p.m_neg23 = 0u - (1u << 23);
   p.m_pos23 = 1u << 23;
   p.sc_bits = (uint32_t)(254 + man_bits) << 23;
@@ -491,28 +495,31 @@ LPQ_HD float quant_float_fast(float x, const FloatParams& p, uint32_t v) {
 }
 
 // Float quantizer, scaled form for NearestEven / Stochastic and
-// 2 <= exp_bits <= 7 (so every scale below is a normal fp32 power of two):
-// the binade exponent E = clamp(e, -, max_exp) (or min_exp + man below the
-// normal range, which makes the grid step 2^min_exp as in the reference's
-// two-point underflow rule) gives r = x * 2^(man - E) exactly, one rounding,
-// q = k * 2^(E - man) exactly, and saturation is a clamp to +-max_value
-// (a carry out of the top binade or e > max_exp lands beyond it).  Zero
-// results are +0 except x == -0 itself, which passes through.  About half the
-// instructions of quant_float_fast; identical results to quant_float<M>.
+// 2 <= exp_bits <= 7 (so every scale below is a normal fp32 power of two).
+// x is first clamped to [-max_value, max_value]: max_value is the top grid
+// point, so every rounding of a clamped value stays within it and every x
+// beyond it saturates to it in all modes (stochastic rounding past max_value
+// lands on the next grid point 2^(max_exp+1), which saturates back) -- no
+// clamp of the exponent from above and none of the result.  The binade
+// exponent E = e (or min_exp + man below the normal range, which makes the
+// grid step 2^min_exp as in the reference's two-point underflow rule) gives
+// r = x * 2^(man - E) exactly, one rounding, q = k * 2^(E - man) + 0 in one
+// FFMA (exact; -0 -> +0).  Zero results are +0 except x == -0 itself, which
+// passes through.  Identical results to quant_float<M>.
 template <int M>
 LPQ_HD float quant_float_scaled(float x, const FloatParams& p, uint32_t v) {
-  const uint32_t xb = f2u(x);
-  // biased exponent, (xb >> 23) & 0xFF as IMAD.HI (runtime 2^9) + LOP3
-  int ef = (int)(umulhi32(xb, p.m_sh9) & 0xFFu);
-  ef = ef < p.ef_min ? p.ef_under : (ef > p.ef_max ? p.ef_max : ef);
+  const float xc = fminf(fmaxf(x, -p.max_value), p.max_value);
+  // biased exponent of |xc| as IMAD (x2 drops the sign) + IMAD.HI (>> 24)
+  // against runtime multipliers, on the FMA pipe
+  int ef = (int)umulhi32(f2u(xc) * p.m_two, p.m_sh8);
+  ef = ef < p.ef_min ? p.ef_under : ef;
   // exponent fields as IMADs against the runtime +-2^23 (FMA pipe):
   // 2^(man - E) and 2^(E - man)
   const float sc = u2f((uint32_t)ef * p.m_neg23 + p.sc_bits);
   const float inv = u2f((uint32_t)ef * p.m_pos23 + p.inv_bits);
-  const float k = round_signed<M>(fmul(x, sc), v);
-  float q = fmul(k, inv);
-  q = fminf(fmaxf(q, -p.max_value), p.max_value);
-  return x == 0.0f ? x : fadd(q, 0.0f);
+  const float k = round_signed<M>(fmul(xc, sc), v);
+  const float q = fma_rn(k, inv, 0.0f);
+  return x == 0.0f ? x : q;
 }
 
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;
