@@ -22,24 +22,41 @@ __device__ __forceinline__ uint32_t nf4(const float4& v) {
 // ends); uniform per block, so kernels branch once per block/row.
 // z = key ^ flat index; m32 == 32 (runtime, see variate24_zb).
 // GUARD: see quant_block_fast (stochastic flush guard; needs_guard()).
+// v: the element's 24-bit variate (stochastic), else unused
 template <int M, bool TWO, bool GUARD = true>
-__device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
-                                    float kmax, uint64_t z, const RngMul& rm) {
-  uint32_t v = 0;
-  if (M == kStochastic) v = variate24_zb(z, rm.m32);
+__device__ __forceinline__ float qbv(float x, const BlockScale& s, float kmin,
+                                     float kmax, uint32_t v, const RngMul& rm) {
   if (M == kNearestEven || M == kStochastic)
     return quant_block_fast<M == kNearestEven ? kNearestEven : kStochastic, TWO,
                             GUARD>(x, s, kmin, kmax, v, rm.m2, rm.neg1);
   return quant_block<M>(x, s, kmin, kmax, v);
 }
 
-// IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q
+template <int M, bool TWO, bool GUARD = true>
+__device__ __forceinline__ float qb(float x, const BlockScale& s, float kmin,
+                                    float kmax, uint64_t z, const RngMul& rm) {
+  uint32_t v = 0;
+  if (M == kStochastic) v = variate24_zb(z, rm.m32);
+  return qbv<M, TWO, GUARD>(x, s, kmin, kmax, v, rm);
+}
+
+// IDX4: idx % 4 == 0, so key ^ (idx + q) == (key ^ idx) ^ q, and the four
+// variates come from variate24_x4
 template <int M, bool TWO, bool IDX4, bool GUARD = true>
 __device__ __forceinline__ float4 qb4(const float4& x, const BlockScale& s,
                                       float kmin, float kmax, uint64_t key,
                                       uint64_t idx, const RngMul& m32) {
-  const uint64_t z0 = key ^ idx;
   float4 o;
+  if (M == kStochastic && IDX4) {
+    uint32_t v[4];
+    variate24_x4(key, idx, m32.m32, v);
+    o.x = qbv<M, TWO, GUARD>(x.x, s, kmin, kmax, v[0], m32);
+    o.y = qbv<M, TWO, GUARD>(x.y, s, kmin, kmax, v[1], m32);
+    o.z = qbv<M, TWO, GUARD>(x.z, s, kmin, kmax, v[2], m32);
+    o.w = qbv<M, TWO, GUARD>(x.w, s, kmin, kmax, v[3], m32);
+    return o;
+  }
+  const uint64_t z0 = key ^ idx;
   o.x = qb<M, TWO, GUARD>(x.x, s, kmin, kmax, z0, m32);
   o.y = qb<M, TWO, GUARD>(x.y, s, kmin, kmax, IDX4 ? z0 ^ 1u : key ^ (idx + 1), m32);
   o.z = qb<M, TWO, GUARD>(x.z, s, kmin, kmax, IDX4 ? z0 ^ 2u : key ^ (idx + 2), m32);

@@ -74,6 +74,13 @@ __device__ __forceinline__ float qelem(const Op& op, float x, uint64_t z,
   return op.template apply<M>(x, v);
 }
 
+template <int M, class Op>
+__device__ __forceinline__ float qelem_v(const Op& op, float x, uint32_t v,
+                                         float& nf) {
+  nf = __fmaf_rn(x, 0.0f, nf);
+  return op.template apply<M>(x, v);
+}
+
 // IDX4: (base + head) % 4 == 0, so the four flat indices of a float4 differ
 // from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
 template <int M, class Op, bool IDX4>
@@ -99,6 +106,17 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t j = i0 + (int64_t)u * kThreads;
       if (j < n4) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
+        if (M == kStochastic && IDX4) {  // the float4's variates together
+          uint32_t vv[4];
+          variate24_x4(key, idx, rm.m32, vv);
+          float4 o;
+          o.x = qelem_v<M>(op, v[u].x, vv[0], nf);
+          o.y = qelem_v<M>(op, v[u].y, vv[1], nf);
+          o.z = qelem_v<M>(op, v[u].z, vv[2], nf);
+          o.w = qelem_v<M>(op, v[u].w, vv[3], nf);
+          __stcs(y4 + j, o);
+          continue;
+        }
         uint64_t z0, z1, z2, z3;
         if (IDX4) {
           z0 = key ^ idx;

@@ -233,6 +233,51 @@ LPQ_HD uint32_t variate24_zf(uint64_t z, const RngMul& m) {
   return umulhi32(top, m.m24);  // top >> 8
 }
 
+// Four variates for the flat indices idx .. idx+3 with idx % 4 == 0 (the
+// four lanes of a float4), sharing the work their hashes have in common.
+// z_q = key ^ (idx + q) = (key ^ idx) ^ q, so z_q + C0 = w + j_q with
+// w = ((key ^ idx) & ~3) + C0 and j_q = (key & 3) ^ q: unless the low word
+// of w is within 3 of 2^32 (then the generic form runs), the four sums share
+// their HIGH word.  That makes the high word of z ^= z >> 30 shared, and the
+// hi * C1lo term of z *= C1 shared; per lane there remain one add, a funnel
+// shift + xor, one IMAD.WIDE + one IMAD, and the unshared tail (>> 27 xor,
+// the last product's high word).  Identical to variate24_z(key ^ (idx + q)).
+LPQ_HD uint32_t funnel_r30(uint32_t lo, uint32_t hi) {
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_r(lo, hi, 30);
+#else
+  return (uint32_t)((((uint64_t)hi << 32) | lo) >> 30);
+#endif
+}
+
+LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
+                         uint32_t out[4]) {
+  const uint64_t z0 = key ^ idx;
+  const uint64_t w = (z0 & ~3ull) + 0x9E3779B97F4A7C15ull;
+  const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
+  const uint32_t kl = (uint32_t)key & 3u;
+  if (wlo > 0xFFFFFFFCu) {  // w + j_q may carry into the high word
+    for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m32);
+    return;
+  }
+  const uint32_t h1 = whi ^ (whi >> 30);                   // shared
+  const uint64_t hc = (uint64_t)(h1 * 0x1CE4E5B9u) << 32;  // shared hi*C1lo
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t lo = wlo + (kl ^ (uint32_t)q);
+    lo ^= funnel_r30(lo, whi);
+    const uint64_t p = (uint64_t)lo * 0x1CE4E5B9u + hc;    // z *= C1
+    uint32_t plo = (uint32_t)p;
+    uint32_t phi = (uint32_t)(p >> 32) + lo * 0xBF58476Du;
+    const uint32_t slo = umulhi32(plo, m32) + phi * m32;   // z ^= z >> 27
+    const uint32_t shi = umulhi32(phi, m32);
+    plo ^= slo;
+    phi ^= shi;
+    const uint32_t top = umulhi32(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
+    out[q] = top >> 8;
+  }
+}
+
 // ---- magnitude rounding ---------------------------------------------------
 //
 // a = |r| where r = x * 2^s was formed in fp32; a is exact unless it fell

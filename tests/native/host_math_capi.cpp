@@ -86,5 +86,9 @@ void hm_variates24_fma(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   const lpq::RngMul m = lpq::rng_mul();
   for (int64_t i = 0; i < n; ++i) out[i] = lpq::variate24_zf(key ^ (base + (uint64_t)i), m);
 }
+// the float4 form (idx % 4 == 0), n a multiple of 4
+void hm_variates24_x4(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  for (int64_t i = 0; i < n; i += 4) lpq::variate24_x4(key, base + (uint64_t)i, 32u, out + i);
+}
 uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
 }

@@ -36,6 +36,7 @@ def hm():
     L.hm_variates24.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_balanced.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_fma.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_variates24_x4.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     return L
 
 
@@ -83,6 +84,24 @@ def test_balanced_variate_form_is_identical(hm):
         assert np.array_equal(a, b)
         hm.hm_variates24_fma(key, base, b.size, b)
         assert np.array_equal(a, b)
+
+
+def test_float4_variate_form_is_identical(hm):
+    # variate24_x4 shares the high word of key ^ (idx + q) + C0 across the 4
+    # lanes; cover its carry fallback (low word of w within 3 of 2^32) too
+    C0 = 0x9E3779B97F4A7C15
+    near = []
+    for d in range(0, 8):  # key ^ idx with (z & ~3) + C0 ending at 2^32 - 1 - d
+        z = ((1 << 32) - 1 - d - (C0 & 0xFFFFFFFF)) & 0xFFFFFFFF | (0x12345 << 32)
+        near.append((z & ~3 & (2**64 - 1), 0))
+    cases = [(0, 0), (0x5E41AB087439611E, 2**40), (2**64 - 1, 2**63), (3, 4), (6, 2**32 - 4)] + near
+    for key, base in cases:
+        n = 1 << 12
+        a = np.empty(n, np.uint32)
+        b = np.empty(n, np.uint32)
+        hm.hm_variates24(key, base, n, a)
+        hm.hm_variates24_x4(key, base, n, b)
+        assert np.array_equal(a, b), (key, base)
 
 
 @pytest.mark.parametrize("fmt", FORMATS, ids=repr)
