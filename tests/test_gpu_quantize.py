@@ -447,3 +447,35 @@ def test_block_nonfinite_every_plan(q, shape, dim, mode):
             q.quantize_fused(dev(xb.reshape(shape)), spec)
     got = q.quantize_fused_at(dev(x), spec, 0)  # status cleared
     assert np.isfinite(got.cpu().numpy()).all()
+
+
+def test_beyond_2p32_elements_windows(q, oracle):
+    # 2^32 + 4100 elements (16 GiB in + out): flat indices past 2^32 feed the
+    # RNG's high key word and every 64-bit index path; windows straddling
+    # 2^31 and 2^32 are checked against the oracle with index_base
+    n = (1 << 32) + 4100
+    x = q.random_uniform((n,), 9, 0, -10.0, 10.0)
+    for fmt, ofmt in ((q.FixedFormat(8, 4), fixed_fmt(8, 4)), (q.FloatFormat(5, 2), float_fmt(5, 2))):
+        spec = q.QuantSpec(fmt, q.RoundingMode.Stochastic, 0x15EED)
+        y = q.quantize_fused_at(x, spec, 7)
+        w = 1 << 16
+        for lo in ((1 << 31) - 999, (1 << 32) - 3 * w // 2, n - w):
+            xs = x[lo:lo + w].cpu().numpy()
+            st, want = oracle.quantize(xs, ofmt, STOCHASTIC, seed=0x15EED, call=7,
+                                       index_base=lo)
+            assert st == 0
+            assert np.array_equal(bits(y[lo:lo + w].cpu().numpy()), bits(want)), (fmt, lo)
+        del y
+    # block rows: n // 4100 rows of 4100 floats (> 2^32 elements in total)
+    rows = n // 4100
+    xb = x[: rows * 4100].view(rows, 4100)
+    spec = q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode.Stochastic, 3)
+    yb = q.quantize_fused_at(xb, spec, 1)
+    for r in (0, (1 << 19) + 7, rows - 2):
+        rows = xb[r:r + 2].cpu().numpy()
+        st, want = oracle.quantize(rows, block_fmt(8, 0), STOCHASTIC, seed=3, call=1,
+                                   index_base=r * 4100)
+        assert st == 0
+        assert np.array_equal(bits(yb[r:r + 2].cpu().numpy()), bits(want)), r
+    del x, xb, yb
+    torch.cuda.empty_cache()
