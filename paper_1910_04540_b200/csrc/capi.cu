@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdint>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -83,10 +84,16 @@ lpq_status check_format(const lpq_format* f) {
 lpq_status check_shape(const int64_t* shape, int rank, int64_t* numel) {
   if (rank < 0 || (rank > 0 && !shape)) return LPQ_ERR_ARGUMENT;
   int64_t n = 1;
+  bool zero = false;
   for (int d = 0; d < rank; ++d) {
     if (shape[d] < 0) return LPQ_ERR_SHAPE;  // tensor.cpp:237-244
+    if (shape[d] == 0) zero = true;
+  }
+  for (int d = 0; d < rank && !zero; ++d) {
+    if (shape[d] > INT64_MAX / 4 / n) return LPQ_ERR_SHAPE;  // bytes overflow int64
     n *= shape[d];
   }
+  if (zero) n = 0;
   *numel = n;
   return LPQ_OK;
 }

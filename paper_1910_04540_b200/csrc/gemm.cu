@@ -29,6 +29,8 @@
 //    because the product of two fp32 values is exact in double.
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include <algorithm>
 #include <cmath>
 #include <memory>
@@ -602,6 +604,13 @@ size_t lpq_quant_gemm_workspace_size(int64_t, int64_t, int64_t) {
   return 256;  // GemmScan, padded
 }
 
+// every operand's byte count fits int64 (A: M x K, B: K x N, C: M x N)
+static bool gemm_dims_ok(int64_t M, int64_t N, int64_t K) {
+  const int64_t lim = INT64_MAX / 4;
+  auto fits = [&](int64_t a, int64_t b) { return a == 0 || b <= lim / a; };
+  return fits(M, K) && fits(K, N) && fits(M, N);
+}
+
 lpq_status lpq_quant_gemm(const float* A, const float* B, float* C, int64_t M,
                           int64_t N, int64_t K, int64_t row_base,
                           const lpq_format* fmul, const lpq_format* fadd,
@@ -613,8 +622,9 @@ lpq_status lpq_quant_gemm(const float* A, const float* B, float* C, int64_t M,
   if (fmul->kind != LPQ_FLOAT || fadd->kind != LPQ_FLOAT) return LPQ_ERR_UNSUPPORTED;
   if (M < 0 || N < 0 || K < 0 || row_base < 0 || mode < 0 || mode > 3)
     return LPQ_ERR_ARGUMENT;
+  if (!gemm_dims_ok(M, N, K)) return LPQ_ERR_SHAPE;
   if (M == 0 || N == 0) return LPQ_OK;
-  if (!A || !B || !C || !d_status || (K > 0 && (!A || !B))) return LPQ_ERR_ARGUMENT;
+  if (!C || !d_status || (K > 0 && (!A || !B))) return LPQ_ERR_ARGUMENT;
   if (!ws || ws_bytes < sizeof(GemmScan)) return LPQ_ERR_WORKSPACE;
   const FloatParams qm = make_float(fmul->exp_bits, fmul->man_bits);
   const FloatParams qa = make_float(fadd->exp_bits, fadd->man_bits);
@@ -636,8 +646,9 @@ lpq_status lpq_matmul_q(const float* A, const float* B, float* C, int64_t M,
   if (st != LPQ_OK) return st;
   if (M < 0 || N < 0 || K < 0 || row_base < 0 || mode < 0 || mode > 3)
     return LPQ_ERR_ARGUMENT;
+  if (!gemm_dims_ok(M, N, K)) return LPQ_ERR_SHAPE;
   if (M == 0 || N == 0) return LPQ_OK;
-  if (!A || !B || !C || !d_status) return LPQ_ERR_ARGUMENT;
+  if (!C || !d_status || (K > 0 && (!A || !B))) return LPQ_ERR_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t key = stream_key(seed, call);
   FloatParams fp{};

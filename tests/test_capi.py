@@ -78,3 +78,23 @@ def test_no_cpu_fallback_without_gpu():
     from paper_1910_04540_b200._lib import DeviceError
     with pytest.raises(DeviceError):
         q.quantize_fused_at(np.ones(16, np.float32), q.QuantSpec(q.FixedFormat(8, 4)), 0)
+
+
+def test_shape_checks_before_any_device_work():
+    # argument and shape errors come back before the library touches a GPU
+    from paper_1910_04540_b200 import _lib
+    import paper_1910_04540_b200 as q
+    f = q.FixedFormat(8, 4).c()
+    L = _lib.lib
+
+    def call(shape):
+        return L.lpq_quantize(None, None, _lib.shape_array(shape), len(shape), 0,
+                              C.byref(f), 0, 0, 0, None, 0, None, None)
+    assert call((1 << 40, 1 << 40)) == _lib.ERR_SHAPE     # element count overflows
+    assert call((1 << 31, 1 << 31)) == _lib.ERR_SHAPE     # byte count overflows
+    assert call((-1, 4)) == _lib.ERR_SHAPE
+    assert call((0, 1 << 62)) == 0                        # empty: nothing to do
+    assert call((4, 4)) == _lib.ERR_ARGUMENT              # null pointers
+    bf = q.BlockFloatFormat(8, 2).c()
+    assert L.lpq_quantize(None, None, _lib.shape_array((4, 4)), 2, 0, C.byref(bf), 0, 0, 0,
+                          None, 0, None, None) == _lib.ERR_SHAPE  # block_dim >= rank

@@ -154,3 +154,16 @@ def test_matmul_q_vs_oracle(q, oracle, M, N, K):
     st, want = oracle.quantize(c, block_fmt(8, 0), NEAREST_EVEN)
     got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(q.BlockFloatFormat(8, 0)), 0)
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_gemm_empty_inner_dimension(q, oracle):
+    # K = 0: every output is the empty sum, +0 (acc starts at +0; the
+    # reference matmul's double accumulator is 0.0, quantized to +0)
+    a = np.zeros((5, 0), np.float32)
+    b = np.zeros((0, 7), np.float32)
+    f87 = q.FloatFormat(8, 7)
+    got = q.quant_gemm(dev(a), dev(b), f87, f87).cpu().numpy()
+    assert got.shape == (5, 7) and np.array_equal(bits(got), np.zeros((5, 7), np.uint32))
+    for fmt in (q.FloatFormat(5, 2), q.FixedFormat(8, 4), q.BlockFloatFormat(8, 0)):
+        got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(fmt), 0).cpu().numpy()
+        assert np.array_equal(bits(got), np.zeros((5, 7), np.uint32)), fmt
