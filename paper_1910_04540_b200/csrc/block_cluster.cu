@@ -27,8 +27,6 @@ namespace {
 
 using namespace blk;
 
-constexpr int64_t kSliceTarget = 65536;  // floats per CTA (sets the cluster size)
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -195,12 +193,19 @@ cudaError_t launch_cluster_m(const float* x, float* y, int64_t L, int64_t nrows,
 
 }  // namespace
 
-// Cluster size for a contiguous block of L floats: ~kSliceTarget floats per
-// CTA, at most 16 CTAs (non-portable cluster size); any L is accepted (very
-// long rows simply have longer slices, and stop fitting in L2).
+// Cluster size for a contiguous block of L floats.  Measured on B200
+// (scripts/time_act_shapes.py, ResNet-50 per-sample activation rows, every
+// cs from 1 to 16): the best sizes are 2 CTAs up to ~100K floats (50176:
+// 4215 GB/s vs 2884 with one CTA), 4 up to ~200K, 8 up to 1M (802816: 4901
+// vs 4048 with 13).  Cluster sizes that tile a GPC's CTA slots well (2, 4,
+// 8: cudaOccupancyMaxActiveClusters, scripts/cluster_probe.cu) beat the
+// "one ~64K-float slice per CTA" rule; longer rows take 128K-float slices.
 int cluster_size_for(int64_t L) {
-  const int64_t cs = (L + kSliceTarget - 1) / kSliceTarget;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(16, cs));
+  if (L <= 110000) return 2;
+  if (L <= 220000) return 4;
+  if (L <= (int64_t(1) << 20)) return 8;
+  const int64_t cs = (L + 131071) / 131072;
+  return (int)std::min<int64_t>(16, cs);
 }
 
 cudaError_t launch_block_cluster(const float* x, float* y, int64_t L,

@@ -138,9 +138,9 @@ BLOCK_CASES = [
     ((64, 100), 0),         # rows, 128 threads
     ((7, 20000), 0),        # rows, 1024 x 8 float4
     ((5, 40000), 0),        # few long rows -> two-pass segments
-    ((300, 40000), 0),      # cluster plan (1 CTA per row)
-    ((80, 200000), 0),      # cluster plan, 4 CTAs per row, DSMEM max exchange
-    ((24, 802816), 0),      # ResNet-50 conv1 per-sample block, 13-CTA clusters
+    ((300, 40000), 0),      # cluster plan, 2 CTAs per row, DSMEM max exchange
+    ((80, 200000), 0),      # cluster plan, 4 CTAs per row
+    ((40, 802816), 0),      # ResNet-50 conv1 per-sample block, 8-CTA clusters
     ((1, 300, 40000), 1),   # cluster plan along dim 1 (leading 1)
     ((4096, 64), 0),        # short rows: 16 lanes per row
     ((999, 12), 0),         # short rows: 4 lanes per row
