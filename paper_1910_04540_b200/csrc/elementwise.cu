@@ -21,7 +21,8 @@ namespace lpq {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 8;  // 8 float4 = 128 B in flight per thread
+constexpr int kUnrollBig = 8;    // 8 float4 = 128 B in flight per thread
+constexpr int kUnrollSmall = 4;  // tensors below 2^26 elements: finer tail
 
 template <bool TINY>
 struct FixedSatOp {
@@ -83,7 +84,7 @@ __device__ __forceinline__ float qelem_v(const Op& op, float x, uint32_t v,
 
 // IDX4: (base + head) % 4 == 0, so the four flat indices of a float4 differ
 // from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
-template <int M, class Op, bool IDX4>
+template <int M, class Op, bool IDX4, int kUnroll>
 __global__ void __launch_bounds__(kThreads)
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
@@ -171,15 +172,23 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   // retire and launch in address order, which keeps the DRAM pages in use
   // compact.  Measured on B200 (scripts/ew_variants.cu, 2^30 elements):
   // persistent grid-stride 5.85 TB/s vs one-trip 8 x float4 6.59 TB/s.
-  const int64_t want = (work + (int64_t)kThreads * kUnroll - 1) /
-                       ((int64_t)kThreads * kUnroll);
+  // tensors below 2^26 elements: 4 float4 per thread, a finer last wave
+  // (graph-captured back-to-back launches, scripts/time_b2b.py: 2^24
+  // float(5,2) nearest 6082 -> 6319 GB/s, 2^20 stochastic 1764 -> 2032)
+  const bool small = idx4 && n < (int64_t(1) << 26);
+  const int unroll = small ? kUnrollSmall : kUnrollBig;
+  const int64_t want = (work + (int64_t)kThreads * unroll - 1) /
+                       ((int64_t)kThreads * unroll);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
-  if (idx4)
-    k_elementwise<M, Op, true><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                         key, op, rng_mul(), status);
+  if (small)
+    k_elementwise<M, Op, true, kUnrollSmall><<<grid, kThreads, 0, s>>>(
+        x, y, n, head, base, key, op, rng_mul(), status);
+  else if (idx4)
+    k_elementwise<M, Op, true, kUnrollBig><<<grid, kThreads, 0, s>>>(
+        x, y, n, head, base, key, op, rng_mul(), status);
   else
-    k_elementwise<M, Op, false><<<grid, kThreads, 0, s>>>(x, y, n, head, base,
-                                                          key, op, rng_mul(), status);
+    k_elementwise<M, Op, false, kUnrollBig><<<grid, kThreads, 0, s>>>(
+        x, y, n, head, base, key, op, rng_mul(), status);
   note_launch();
   return cudaGetLastError();
 }
