@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -146,29 +147,106 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Persistent copy workers for parallel_memcpy (spawning threads per call
+// cost more than a 4 MB copy).  Parts of >= 512 KB, at most 16 threads
+// including the caller.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  int width() const { return (int)workers_.size() + 1; }
+
+  void run(char* dst, const char* src, size_t bytes, int parts) {
+    const size_t part = (bytes / parts + 63) & ~size_t(63);
+    std::unique_lock<std::mutex> lk(mu_);
+    jobs_.clear();
+    for (int t = 1; t < parts; ++t) {
+      const size_t b = part * t;
+      if (b >= bytes) break;
+      jobs_.push_back(Job{dst + b, src + b, std::min(part, bytes - b)});
+    }
+    next_ = 0;
+    pending_ = jobs_.size();
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(part, bytes));
+    lk.lock();
+    // help with whatever the workers have not picked up, then wait
+    while (next_ < jobs_.size()) {
+      const Job j = jobs_[next_++];
+      lk.unlock();
+      std::memcpy(j.dst, j.src, j.len);
+      lk.lock();
+      --pending_;
+    }
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  struct Job {
+    char* dst;
+    const char* src;
+    size_t len;
+  };
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int n = (int)std::max(1u, std::min(hw, 16u)) - 1;
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < jobs_.size()); });
+      if (stop_) return;
+      while (next_ < jobs_.size()) {
+        const Job j = jobs_[next_++];
+        lk.unlock();
+        std::memcpy(j.dst, j.src, j.len);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+      seen = gen_;
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::vector<Job> jobs_;
+  size_t next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+std::mutex g_copy_mu;  // one parallel copy at a time (the pool is shared)
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  const size_t kMin = size_t(8) << 20;
-  unsigned hw = std::thread::hardware_concurrency();
-  const int T = (int)std::min<size_t>(std::max(1u, std::min(hw, 16u)),
-                                      std::max<size_t>(1, bytes / kMin));
-  if (T <= 1) {
+  // below 8 MB the workers' wake-up costs more than the copy
+  const size_t kMinPart = size_t(1) << 20;
+  const size_t want = bytes < (size_t(8) << 20) ? 1 : bytes / kMinPart;
+  if (want <= 1) {
     std::memcpy(dst, src, bytes);
     return;
   }
-  const size_t part = (bytes / T + 63) & ~size_t(63);
-  std::vector<std::thread> pool;
-  pool.reserve(T - 1);
-  for (int t = 1; t < T; ++t) {
-    const size_t b = part * t;
-    if (b >= bytes) break;
-    const size_t len = std::min(part, bytes - b);
-    pool.emplace_back([=] {
-      std::memcpy(static_cast<char*>(dst) + b,
-                  static_cast<const char*>(src) + b, len);
-    });
+  std::lock_guard<std::mutex> lk(g_copy_mu);
+  CopyPool& pool = CopyPool::get();
+  const int parts = (int)std::min<size_t>(want, (size_t)pool.width());
+  if (parts <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
   }
-  std::memcpy(dst, src, std::min(part, bytes));
-  for (auto& th : pool) th.join();
+  pool.run(static_cast<char*>(dst), static_cast<const char*>(src), bytes, parts);
 }
 
 int resolve_device(int device, lpq_status* st) {
@@ -299,6 +377,31 @@ lpq_status resident_quantize(HostCtx* c, const float* x, float* y,
   return lpq_status_fetch(c->d_status, s);
 }
 
+// Small tensors (<= 16 MB): one copy in, the device call, one copy out on
+// one stream; the driver stages pageable memory itself.  Below ~16 MB the
+// chunked pipeline's per-chunk events, waits and bounce copies cost more
+// than the overlap they buy (scripts/time_host.py).
+lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
+                           const int64_t* shape, int rank, int64_t n,
+                           uint64_t index_base, const lpq_format* f, int mode,
+                           uint64_t seed, uint64_t call) {
+  LPQ_TRY(c->ensure_full(n));
+  const size_t wsb = lpq_workspace_size(f, shape, rank);
+  if (wsb) LPQ_TRY(c->ensure_ws(wsb));
+  cudaStream_t s = c->st[0];
+  const size_t bytes = sizeof(float) * (size_t)n;
+  LPQ_TRY(cudaMemcpyAsync(c->dfull, x, bytes, cudaMemcpyHostToDevice, s));
+  const lpq_status qst = quantize_device(c->dfull, c->dfull, shape, rank, index_base,
+                                         f, mode, seed, call, c->ws, c->ws_bytes,
+                                         c->d_status, s);
+  if (qst != LPQ_OK) {
+    cudaStreamSynchronize(s);
+    return qst;
+  }
+  LPQ_TRY(cudaMemcpyAsync(y, c->dfull, bytes, cudaMemcpyDeviceToHost, s));
+  return lpq_status_fetch(c->d_status, s);
+}
+
 }  // namespace
 
 lpq_status host_context_quantize(const float* x, float* y,
@@ -326,6 +429,8 @@ lpq_status host_context_quantize(const float* x, float* y,
   std::lock_guard<std::mutex> lk(c->mu);
   cudaError_t e = c->init();
   if (e != cudaSuccess) return cuda_fail(e);
+  if ((int64_t)sizeof(float) * n <= (int64_t(16) << 20))
+    return direct_quantize(c, x, y, shape, rank, n, index_base, f, mode, seed, call);
   if (f->kind != LPQ_BLOCK)
     return stream_quantize(c, x, y, n, 1, false, index_base, f, mode, seed, call);
   // an aligned device buffer decides the plan exactly as the device call will
