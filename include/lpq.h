@@ -218,6 +218,34 @@ lpq_status lpq_sgd_step(const float* grad, float* vel, float* acc,
                         const lpq_quant_slot* weight_q, uint64_t index_base,
                         uint32_t* d_status, void* stream);
 
+/* One parameter tensor of a grouped optimizer step: device pointers, its
+ * element count and flat-index base, and the call id of each of its four
+ * quantizations (gradient, accumulator on the velocity, accumulator on the
+ * accumulator, weight) -- the values the reference's per-parameter loop
+ * would use (train.cpp:148-178 advances each stochastic spec per tensor). */
+typedef struct {
+  const float* grad;
+  float* vel;
+  float* acc;
+  float* weight;
+  int64_t n;
+  uint64_t index_base;
+  uint64_t call_grad, call_vel, call_acc, call_weight;
+} lpq_sgd_tensor;
+
+/* LowPrecisionOptimizer::step over `count` parameter tensors in as few
+ * launches as possible (up to 64 tensors per launch; the tensor table
+ * travels in the kernel parameters, so the call is graph-capturable).  Same
+ * per-element semantics as lpq_sgd_step; the slots' `call` fields are
+ * ignored in favour of each tensor's call ids. */
+lpq_status lpq_sgd_step_grouped(const lpq_sgd_tensor* tensors, int count,
+                                float momentum, float lr,
+                                const lpq_quant_slot* grad_q,
+                                const lpq_quant_slot* acc_q_vel,
+                                const lpq_quant_slot* acc_q_acc,
+                                const lpq_quant_slot* weight_q,
+                                uint32_t* d_status, void* stream);
+
 /* ---- host entry points (synchronous; host buffers) ---------------------- */
 
 /* quantize_fused_at over host memory on CUDA device `device` (-1 = current):

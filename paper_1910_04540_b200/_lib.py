@@ -77,6 +77,14 @@ class LpqTensorDesc(C.Structure):
                 ("call", C.c_uint64)]
 
 
+class LpqSgdTensor(C.Structure):
+    """lpq_sgd_tensor (include/lpq.h)."""
+    _fields_ = [("grad", C.c_void_p), ("vel", C.c_void_p), ("acc", C.c_void_p),
+                ("weight", C.c_void_p), ("n", C.c_int64), ("index_base", C.c_uint64),
+                ("call_grad", C.c_uint64), ("call_vel", C.c_uint64),
+                ("call_acc", C.c_uint64), ("call_weight", C.c_uint64)]
+
+
 _F = C.POINTER(LpqFormat)
 _S = C.POINTER(LpqQuantSlot)
 _I64P = C.POINTER(C.c_int64)
@@ -127,6 +135,8 @@ _PROTOS = {
     "lpq_sgd_step": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, C.c_float,
                                C.c_float, _S, _S, _S, _S, C.c_uint64, _VP,
                                _VP]),
+    "lpq_sgd_step_grouped": (C.c_int, [C.POINTER(LpqSgdTensor), C.c_int, C.c_float,
+                                       C.c_float, _S, _S, _S, _S, _VP, _VP]),
     "lpq_quantize_grouped": (C.c_int, [C.POINTER(LpqTensorDesc), C.c_int, _F,
                                        C.c_int, C.c_uint64, _VP, C.c_size_t,
                                        _VP, _VP]),

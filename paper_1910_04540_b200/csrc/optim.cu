@@ -41,24 +41,57 @@ struct Slot {
   FixedParams xp;
 };
 
+// The element forms the streaming quantizers use (elementwise.cu launch_*),
+// picked by the slot's (uniform) parameters.
 template <int M>
 __device__ __forceinline__ float q_mode(float x, const Slot& s, uint32_t v) {
-  if (s.kind == LPQ_FLOAT) return quant_float<M>(x, s.fp, v);
-  if (s.saturate) return quant_fixed<M, true>(x, s.xp, v);
+  constexpr bool kFast = M == kNearestEven || M == kStochastic;
+  if (s.kind == LPQ_FLOAT) {
+    if (kFast && s.fp.scaled_ok) return quant_float_scaled<kFast ? M : kNearestEven>(x, s.fp, v);
+    if (kFast && !s.fp.tiny) return quant_float_fast<kFast ? M : kNearestEven>(x, s.fp, v);
+    return quant_float<M>(x, s.fp, v);
+  }
+  if (s.saturate) {
+    if (s.xp.tiny) return quant_fixed<M, true, true>(x, s.xp, v);
+    return quant_fixed_sat_fast<M>(x, s.xp, v);
+  }
   return quant_fixed<M, false>(x, s.xp, v);
 }
 
 // grid-uniform dispatch on the slot's mode (no divergence)
-__device__ __forceinline__ float q_slot(float x, const Slot& s, uint64_t idx,
-                                        uint32_t& flags) {
+__device__ __forceinline__ float q_slot_key(float x, const Slot& s, uint64_t key,
+                                            uint64_t idx, uint32_t& flags) {
   if (!s.enabled) return x;
   if (nonfinite(x)) flags |= kStatusNonFinite;
   switch (s.mode) {
-    case kStochastic: return q_mode<kStochastic>(x, s, variate24(s.key, idx));
+    case kStochastic: return q_mode<kStochastic>(x, s, variate24(key, idx));
     case kNearestAway: return q_mode<kNearestAway>(x, s, 0u);
     case kNearestZero: return q_mode<kNearestZero>(x, s, 0u);
     default: return q_mode<kNearestEven>(x, s, 0u);
   }
+}
+
+__device__ __forceinline__ float q_slot(float x, const Slot& s, uint64_t idx,
+                                        uint32_t& flags) {
+  return q_slot_key(x, s, s.key, idx, flags);
+}
+
+// LowPrecisionOptimizer::step (train.cpp:148-178) for one element
+__device__ __forceinline__ void sgd_element(float gin, float& vel, float& acc,
+                                            float& w, float momentum, float lr,
+                                            const Slot* q, const uint64_t* key,
+                                            uint64_t idx, uint32_t& flags) {
+  const float g = q_slot_key(gin, q[0], key[0], idx, flags);
+  float v = __fadd_rn(__fmul_rn(momentum, vel), g);  // add(scale(vel, m), g)
+  if (nonfinite(v)) flags |= kStatusInvalidValue;    // map_elements check
+  v = q_slot_key(v, q[1], key[1], idx, flags);
+  vel = v;
+  const float lv = __fmul_rn(v, lr);                  // scale(v, lr)
+  float a = __fsub_rn(acc, lv);                       // sub(acc, .)
+  if (nonfinite(lv) || nonfinite(a)) flags |= kStatusInvalidValue;
+  a = q_slot_key(a, q[2], key[2], idx, flags);
+  acc = a;
+  w = q_slot_key(a, q[3], key[3], idx, flags);
 }
 
 __global__ void __launch_bounds__(kT)
@@ -81,6 +114,66 @@ __global__ void __launch_bounds__(kT)
     a = q_slot(a, qa2, idx, flags);
     acc[i] = a;
     w[i] = q_slot(a, qw, idx, flags);
+  }
+  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
+}
+
+// ---- grouped step: many parameter tensors per launch ----------------------
+constexpr int kMaxSgd = 64;
+constexpr int kSgdPer = 4;                 // elements per thread
+constexpr int64_t kSgdTile = (int64_t)kT * kSgdPer;
+
+struct SgdEntry {
+  const float* g;
+  float* v;
+  float* a;
+  float* w;
+  int64_t n;
+  uint64_t base;
+  uint64_t key[4];
+  int64_t first;  // first CTA of this tensor
+};
+
+struct SgdTable {
+  SgdEntry e[kMaxSgd];
+  Slot q[4];
+  int count;
+  int64_t ctas;
+};
+
+__global__ void __launch_bounds__(kT)
+    k_sgd_grouped(const __grid_constant__ SgdTable t, float momentum, float lr,
+                  uint32_t* __restrict__ status) {
+  int lo = 0, hi = t.count - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.e[mid].first <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const SgdEntry& e = t.e[lo];
+  const int64_t t0 = ((int64_t)blockIdx.x - e.first) * kSgdTile;
+  uint32_t flags = 0;
+  float gv[kSgdPer], vv[kSgdPer], av[kSgdPer];
+#pragma unroll
+  for (int k = 0; k < kSgdPer; ++k) {  // all loads first (coalesced)
+    const int64_t i = t0 + threadIdx.x + (int64_t)k * kT;
+    if (i < e.n) {
+      gv[k] = __ldcs(e.g + i);
+      vv[k] = __ldcs(e.v + i);
+      av[k] = __ldcs(e.a + i);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kSgdPer; ++k) {
+    const int64_t i = t0 + threadIdx.x + (int64_t)k * kT;
+    if (i < e.n) {
+      float w;
+      sgd_element(gv[k], vv[k], av[k], w, momentum, lr, t.q, e.key,
+                  e.base + (uint64_t)i, flags);
+      __stcs(e.v + i, vv[k]);
+      __stcs(e.a + i, av[k]);
+      __stcs(e.w + i, w);
+    }
   }
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
@@ -137,5 +230,59 @@ extern "C" lpq_status lpq_sgd_step(const float* grad, float* vel, float* acc,
   note_launch();
   note_passes(1);
   const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
+}
+
+extern "C" lpq_status lpq_sgd_step_grouped(const lpq_sgd_tensor* tensors,
+                                           int count, float momentum, float lr,
+                                           const lpq_quant_slot* grad_q,
+                                           const lpq_quant_slot* acc_q_vel,
+                                           const lpq_quant_slot* acc_q_acc,
+                                           const lpq_quant_slot* weight_q,
+                                           uint32_t* d_status, void* stream) {
+  if (count < 0 || (count > 0 && !tensors)) return LPQ_ERR_ARGUMENT;
+  SgdTable t{};
+  const lpq_quant_slot* in[4] = {grad_q, acc_q_vel, acc_q_acc, weight_q};
+  for (int k = 0; k < 4; ++k) {
+    lpq_status st = make_slot(in[k], &t.q[k]);
+    if (st != LPQ_OK) return st;
+  }
+  for (int i = 0; i < count; ++i) {
+    const lpq_sgd_tensor& d = tensors[i];
+    if (d.n < 0) return LPQ_ERR_ARGUMENT;
+    if (d.n > 0 && (!d.grad || !d.vel || !d.acc || !d.weight)) return LPQ_ERR_ARGUMENT;
+  }
+  if (!d_status) return LPQ_ERR_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto flush = [&]() -> cudaError_t {
+    if (t.count == 0) return cudaSuccess;
+    k_sgd_grouped<<<(unsigned)t.ctas, kT, 0, s>>>(t, momentum, lr, d_status);
+    note_launch();
+    note_passes(1);
+    t.count = 0;
+    t.ctas = 0;
+    return cudaGetLastError();
+  };
+  for (int i = 0; i < count; ++i) {
+    const lpq_sgd_tensor& d = tensors[i];
+    if (d.n == 0) continue;
+    if (t.count == kMaxSgd) {
+      const cudaError_t e = flush();
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+    SgdEntry& e = t.e[t.count++];
+    e.g = d.grad;
+    e.v = d.vel;
+    e.a = d.acc;
+    e.w = d.weight;
+    e.n = d.n;
+    e.base = d.index_base;
+    const uint64_t calls[4] = {d.call_grad, d.call_vel, d.call_acc, d.call_weight};
+    for (int k = 0; k < 4; ++k)
+      e.key[k] = t.q[k].enabled ? stream_key(in[k]->seed, calls[k]) : 0u;
+    e.first = t.ctas;
+    t.ctas += (d.n + kSgdTile - 1) / kSgdTile;
+  }
+  const cudaError_t e = flush();
   return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
 }

@@ -11,10 +11,12 @@ from __future__ import annotations
 
 import copy
 import ctypes as C
+
+import numpy as np
 from typing import Optional, Sequence
 
 from . import _lib
-from ._lib import FormatError, LpqQuantSlot, ShapeError, check, lib
+from ._lib import FormatError, LpqQuantSlot, LpqSgdTensor, ShapeError, check, lib
 from .quant import QuantSpec, RoundingMode, _status_buf, _stream_ptr, fetch_status
 
 
@@ -33,6 +35,17 @@ def _slot(spec: Optional[QuantSpec], call_offset: int = 0) -> LpqQuantSlot:
 def _advance(spec: Optional[QuantSpec], k: int) -> None:
     if spec is not None and spec.mode == RoundingMode.Stochastic:
         spec.call_counter += k
+
+
+def _sgd_dtype():
+    return np.dtype({"names": [n for n, _ in LpqSgdTensor._fields_],
+                     "formats": [np.uint64 if t is not C.c_int64 else np.int64
+                                 for _, t in LpqSgdTensor._fields_],
+                     "offsets": [getattr(LpqSgdTensor, n).offset for n, _ in LpqSgdTensor._fields_],
+                     "itemsize": C.sizeof(LpqSgdTensor)})
+
+
+_SGD_DTYPE = _sgd_dtype()
 
 
 class LowPrecisionOptimizer:
@@ -69,30 +82,52 @@ class LowPrecisionOptimizer:
         return self.acc
 
     def step(self, grads: Sequence) -> None:
-        """LowPrecisionOptimizer::step (train.cpp:148-178)."""
+        """LowPrecisionOptimizer::step (train.cpp:148-178): every parameter's
+        update in one grouped launch (lpq_sgd_step_grouped, up to 64 tensors
+        per launch), with the call ids the reference's per-parameter loop
+        would give each of its four quantizations."""
         if len(grads) != len(self.params):
             raise ShapeError("optimizer step: gradient count mismatch")
-        for p, g, a, v in zip(self.params, grads, self.acc, self.vel):
+        if not self.params:
+            return
+        acc_stoch = self.acc_spec is not None and self.acc_spec.mode == RoundingMode.Stochastic
+        for p, g in zip(self.params, grads):  # validate before any state changes
             if tuple(p.shape) != tuple(g.shape):
                 raise ShapeError("optimizer step: gradient shape mismatch")
             if not p.is_contiguous():
                 raise ValueError("parameters must be contiguous")
-            g = g.contiguous()
-            acc_stoch = self.acc_spec is not None and self.acc_spec.mode == RoundingMode.Stochastic
-            qg = _slot(self.grad_spec)
-            qv = _slot(self.acc_spec)
-            qa = _slot(self.acc_spec, 1 if acc_stoch else 0)
-            qw = _slot(self.weight_spec)
-            dev = p.device
-            st = lib.lpq_sgd_step(
-                C.c_void_p(g.data_ptr()), C.c_void_p(v.data_ptr()),
-                C.c_void_p(a.data_ptr()), C.c_void_p(p.data_ptr()), p.numel(),
-                self.momentum, self.lr, C.byref(qg), C.byref(qv), C.byref(qa),
-                C.byref(qw), 0, C.c_void_p(_status_buf(dev).data_ptr()),
-                _stream_ptr(dev))
-            check(st, "optimizer step")
-            _advance(self.grad_spec, 1)
-            _advance(self.acc_spec, 2)
-            _advance(self.weight_spec, 1)
-        if self.params:
-            fetch_status(self.params[0].device)
+        # the tensor table, filled column-wise (the per-step host cost of
+        # a Python loop over ctypes structs exceeds the kernel's)
+        cnt = len(self.params)
+        if getattr(self, "_table", None) is None:
+            self._table = np.zeros(cnt, dtype=_SGD_DTYPE)
+            self._table["vel"] = [v.data_ptr() for v in self.vel]
+            self._table["acc"] = [a.data_ptr() for a in self.acc]
+            self._table["weight"] = [p.data_ptr() for p in self.params]
+            self._table["n"] = [p.numel() for p in self.params]
+        t = self._table
+        gs = [g if g.is_contiguous() else g.contiguous() for g in grads]
+        t["grad"] = [g.data_ptr() for g in gs]
+        j = np.arange(cnt, dtype=np.uint64)
+
+        def calls(spec, per):
+            if spec is None:
+                return np.zeros(cnt, np.uint64)
+            step = per if spec.mode == RoundingMode.Stochastic else 0
+            return np.uint64(spec.call_counter) + j * np.uint64(step)
+        t["call_grad"] = calls(self.grad_spec, 1)
+        t["call_vel"] = calls(self.acc_spec, 2)
+        t["call_acc"] = t["call_vel"] + np.uint64(1 if acc_stoch else 0)
+        t["call_weight"] = calls(self.weight_spec, 1)
+        _advance(self.grad_spec, cnt)
+        _advance(self.acc_spec, 2 * cnt)
+        _advance(self.weight_spec, cnt)
+        descs = t.ctypes.data_as(C.POINTER(LpqSgdTensor))
+        dev = self.params[0].device
+        qg, qv, qw = _slot(self.grad_spec), _slot(self.acc_spec), _slot(self.weight_spec)
+        st = lib.lpq_sgd_step_grouped(descs, len(self.params), self.momentum, self.lr,
+                                      C.byref(qg), C.byref(qv), C.byref(qv), C.byref(qw),
+                                      C.c_void_p(_status_buf(dev).data_ptr()),
+                                      _stream_ptr(dev))
+        check(st, "optimizer step")
+        fetch_status(dev)
