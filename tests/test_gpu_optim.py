@@ -56,6 +56,19 @@ class RefOpt:
 
 @pytest.mark.parametrize("cfg", ["wage_like", "float_all_stoch", "no_quant", "nearest_away"])
 def test_sgd_step_matches_reference_semantics(oracle, cfg):
+    run_cfg(oracle, cfg, [(64, 33), (33,), (10, 64), (10,)])
+
+
+def test_sgd_step_many_tensors(oracle):
+    # > 64 tensors: several grouped launches; empty and 1-element tensors;
+    # per-tensor call ids continue across the launch boundary
+    rng = np.random.default_rng(9)
+    shapes = [(int(rng.integers(1, 700)),) for _ in range(66)] + [(0,), (1,), (3, 1025)]
+    run_cfg(oracle, "float_all_stoch", shapes, steps=2)
+    run_cfg(oracle, "wage_like", shapes, steps=2)
+
+
+def run_cfg(oracle, cfg, shapes, steps=4):
     import paper_1910_04540_b200 as q
     from paper_1910_04540_b200.optim import LowPrecisionOptimizer
     S, E = q.RoundingMode.Stochastic, q.RoundingMode.NearestEven
@@ -72,7 +85,6 @@ def test_sgd_step_matches_reference_semantics(oracle, cfg):
                                                   q.RoundingMode.NearestTowardZero)),
     }[cfg]
     rng = np.random.default_rng(5)
-    shapes = [(64, 33), (33,), (10, 64), (10,)]
     params = [rng.uniform(-0.5, 0.5, s).astype(np.float32) for s in shapes]
     dev_params = [torch.from_numpy(p.copy()).cuda() for p in params]
     opt = LowPrecisionOptimizer(dev_params, lr=0.05, momentum=0.9, **specs)
@@ -80,7 +92,7 @@ def test_sgd_step_matches_reference_semantics(oracle, cfg):
     ref = RefOpt(oracle, params, 0.05, 0.9, copy.deepcopy(specs.get("weight")),
                  copy.deepcopy(specs.get("accumulator")), copy.deepcopy(specs.get("gradient")))
     host_params = params
-    for step in range(4):
+    for step in range(steps):
         grads = [rng.normal(0, 0.1, s).astype(np.float32) for s in shapes]
         host_params = ref.step(host_params, grads)
         opt.step([torch.from_numpy(g).cuda() for g in grads])
