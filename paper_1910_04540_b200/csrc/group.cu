@@ -58,16 +58,25 @@ __device__ __forceinline__ int find_entry(const Table& t, int64_t b) {
   return lo;
 }
 
+// the streaming element forms of elementwise.cu, picked by the (uniform)
+// format parameters
 struct FixOp {
   FixedParams p;
   template <int M> __device__ __forceinline__ float apply(float x, uint32_t v) const {
-    if (p.saturate) return quant_fixed<M, true>(x, p, v);
+    if (p.saturate) {
+      if (p.tiny) return quant_fixed<M, true, true>(x, p, v);
+      return quant_fixed_sat_fast<M>(x, p, v);
+    }
     return quant_fixed<M, false>(x, p, v);
   }
 };
 struct FltOp {
   FloatParams p;
   template <int M> __device__ __forceinline__ float apply(float x, uint32_t v) const {
+    constexpr bool kFast = M == kNearestEven || M == kStochastic;
+    constexpr int MF = kFast ? M : kNearestEven;
+    if (kFast && p.scaled_ok) return quant_float_scaled<MF>(x, p, v);
+    if (kFast && !p.tiny) return quant_float_fast<MF>(x, p, v);
     return quant_float<M>(x, p, v);
   }
 };
@@ -90,6 +99,7 @@ __global__ void __launch_bounds__(kT)
     float4 v[kEwU];
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) v[u] = __ldcs(x4 + threadIdx.x + u * kT);
+    const bool idx4 = (e.base & 3u) == 0;  // uniform per tensor
 #pragma unroll
     for (int u = 0; u < kEwU; ++u) {
       const int64_t j = threadIdx.x + u * kT;
@@ -97,12 +107,19 @@ __global__ void __launch_bounds__(kT)
       float4 o;
       const float* vi = reinterpret_cast<const float*>(&v[u]);
       float* oi = reinterpret_cast<float*>(&o);
+      uint32_t r[4] = {0u, 0u, 0u, 0u};
+      if (M == kStochastic) {
+        if (idx4) {
+          variate24_x4(e.key, idx, 32u, r);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) r[q] = variate24(e.key, idx + q);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint32_t r = 0;
-        if (M == kStochastic) r = variate24(e.key, idx + q);
         nf = __fmaf_rn(vi[q], 0.0f, nf);
-        oi[q] = op.template apply<M>(vi[q], r);
+        oi[q] = op.template apply<M>(vi[q], r[q]);
       }
       __stcs(y4 + j, o);
     }
