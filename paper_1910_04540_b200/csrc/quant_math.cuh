@@ -242,11 +242,24 @@ LPQ_HD uint32_t variate24_zf(uint64_t z, const RngMul& m) {
 // hi * C1lo term of z *= C1 shared; per lane there remain one add, a funnel
 // shift + xor, one IMAD.WIDE + one IMAD, and the unshared tail (>> 27 xor,
 // the last product's high word).  Identical to variate24_z(key ^ (idx + q)).
-LPQ_HD uint32_t funnel_r30(uint32_t lo, uint32_t hi) {
+template <int S>
+LPQ_HD uint32_t funnel_r(uint32_t lo, uint32_t hi) {  // (hi:lo >> S).lo, one SHF.R.W
 #if defined(__CUDA_ARCH__)
-  return __funnelshift_r(lo, hi, 30);
+  return __funnelshift_r(lo, hi, S);
 #else
-  return (uint32_t)((((uint64_t)hi << 32) | lo) >> 30);
+  return (uint32_t)((((uint64_t)hi << 32) | lo) >> S);
+#endif
+}
+
+// high word of a * b kept as its own IMAD.HI (no 64-bit addend pair, which
+// costs a register move to zero its low half)
+LPQ_HD uint32_t mulhi_sep(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
 
@@ -265,7 +278,7 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t lo = wlo + (kl ^ (uint32_t)q);
-    lo ^= funnel_r30(lo, whi);
+    lo ^= funnel_r<30>(lo, whi);
     const uint64_t p = (uint64_t)lo * 0x1CE4E5B9u + hc;    // z *= C1
     uint32_t plo = (uint32_t)p;
     uint32_t phi = (uint32_t)(p >> 32) + lo * 0xBF58476Du;
@@ -273,11 +286,11 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
     // xors; the IMAD.HI form of variate24_zb is one instruction longer, and
     // with the shared work gone this kernel is issue-bound, not ALU-bound:
     // C2 6645 -> 6873 GB/s, C3 stochastic 6101 -> 6409)
-    const uint32_t slo = (uint32_t)((((uint64_t)phi << 32) | plo) >> 27);
+    const uint32_t slo = funnel_r<27>(plo, phi);
     const uint32_t shi = phi >> 27;
     plo ^= slo;
     phi ^= shi;
-    const uint32_t top = umulhi32(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
+    const uint32_t top = mulhi_sep(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
     out[q] = top >> 8;
   }
 }
