@@ -571,14 +571,12 @@ LPQ_HD float quant_float_fast(float x, const FloatParams& p, uint32_t v) {
 template <int M>
 LPQ_HD float quant_float_scaled(float x, const FloatParams& p, uint32_t v) {
   const float xc = fminf(fmaxf(x, -p.max_value), p.max_value);
-  // biased exponent of |xc| as IMAD (x2 drops the sign) + IMAD.HI (>> 24)
-  // against runtime multipliers, on the FMA pipe
-  int ef = (int)umulhi32(f2u(xc) * p.m_two, p.m_sh8);
-  ef = ef < p.ef_min ? p.ef_under : ef;
-  // exponent fields as IMADs against the runtime +-2^23 (FMA pipe):
-  // 2^(man - E) and 2^(E - man)
-  const float sc = u2f((uint32_t)ef * p.m_neg23 + p.sc_bits);
-  const float inv = u2f((uint32_t)ef * p.m_pos23 + p.inv_bits);
+  // the exponent field of |xc| in place (no shifts): 2^(man - E) and
+  // 2^(E - man) are one integer add each on it
+  uint32_t eb = f2u(xc) & 0x7F800000u;
+  eb = eb < ((uint32_t)p.ef_min << 23) ? ((uint32_t)p.ef_under << 23) : eb;
+  const float sc = u2f(p.sc_bits - eb);
+  const float inv = u2f(eb + p.inv_bits);
   const float k = round_signed<M>(fmul(xc, sc), v);
   const float q = fma_rn(k, inv, 0.0f);
   return x == 0.0f ? x : q;
