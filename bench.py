@@ -506,6 +506,9 @@ def run_gemm(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
+FP64_DMMA_PEAK = 37.1  # TFLOP/s, scripts/dmma_rate.cu on the round-1 B200
+
+
 def run_matmul_q(args, rank, world, local_rank):
     """The reference's quantized_matmul (quant_ops.cpp:191-193) at 4096^3:
     double-accumulated matmul in ascending k with fixed(8,4) stochastic
@@ -552,9 +555,12 @@ def run_matmul_q(args, rank, world, local_rank):
         "data": "synthetic", "config": {"workload": "quantized_matmul 4096^3, fixed(8,4) stochastic",
                                         "parallelism": f"shard{world}"},
         "gpu_launches": q.launch_count() - l0,
-        "roofline": {"bound": "fp64", "achieved": round(ach, 2), "unit": "TFLOP/s",
-                     "peak": None, "frac": None, "traffic": None,
-                     "peak_source": "no measured FP64 peak in MEASURED_PEAKS.json"},
+        "roofline": {"bound": "fp64 tensor (DMMA)", "achieved": round(ach, 2), "unit": "TFLOP/s",
+                     "peak": FP64_DMMA_PEAK, "frac": round(ach / FP64_DMMA_PEAK, 4),
+                     "traffic": None,
+                     "peak_source": "measured in-repo: register-resident DMMA m8n8k4 loop on "
+                                    "this B200 (scripts/dmma_rate.cu; DFMA: 33.4); "
+                                    "MEASURED_PEAKS.json has no FP64 figure"},
         "clocks": clk.summary(),
     }
 

@@ -382,13 +382,24 @@ void launch_general(const float* A, const float* B, float* C, int64_t M,
 }
 
 // ---------------------------------------------------------------------------
-// k_matmul_q: the reference quantized_matmul, DFMA accumulation in ascending
-// k with the quantizer in the epilogue.  128x128 CTA tile, 256 threads, 8x8
-// double accumulators per thread (rows ty*4+{0..3} and 64+ty*4+{0..3}, same
-// for columns, so a warp's shared-memory reads are contiguous), K staged by 8
-// as double in double-buffered shared memory, the next tile's global loads
-// issued before the current tile's math.
-constexpr int kDM = 128, kDN = 128, kDK = 8, kDT = 256;
+// k_matmul_q: the reference quantized_matmul with the quantizer in the
+// epilogue, accumulated on the FP64 tensor cores.  One DMMA m8n8k4 computes
+// D = C + A*B as the chain fma(a3,b3, fma(a2,b2, fma(a1,b1, fma(a0,b0,c)))) in
+// ascending k -- measured on B200 over 1.3e8 adversarial outputs
+// (scripts/dmma_probe.cu: 0 differences from the DFMA chain, ~20 % from a
+// single-rounding sum) -- and the products of fp32 operands are exact in
+// double, so chaining the MMAs over k in ascending order is bit-identical to
+// the reference's `acc += double(a) * double(b)` (tensor.cpp:355-376).
+// Padding k beyond K adds +-0 products, which leave a (never -0) accumulator
+// unchanged.  128x128 CTA tile, 8 warps of 64x32 (8x4 MMA tiles, 64 double
+// accumulators per thread), K staged by 16 as double in double-buffered
+// shared memory with conflict-free padded strides; 0.375 B of shared-memory
+// traffic per MAC instead of the CUDA-core DFMA tile's 2 B (which capped it at
+// 17.4 TFLOP/s, smem-bandwidth-bound).
+constexpr int kDM = 128, kDN = 128, kDK = 16, kDT = 256;
+constexpr int kDAS = kDK + 4;   // A row stride (doubles): conflict-free fragments
+constexpr int kDBS = kDN + 4;   // B row stride (doubles)
+constexpr size_t kDSmem = sizeof(double) * 2 * ((size_t)kDM * kDAS + (size_t)kDK * kDBS);
 
 struct EpilogueFloat {
   FloatParams p;
@@ -422,81 +433,79 @@ __global__ void __launch_bounds__(kDT)
                float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                int64_t row_base, Epi epi, uint64_t key,
                uint32_t* __restrict__ status) {
-  __shared__ __align__(16) double As[2][kDK][kDM];
-  __shared__ __align__(16) double Bs[2][kDK][kDN];
-  const int t = threadIdx.x;
-  const int tx = t & 15, ty = t >> 4;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                              // [2][kDM][kDAS]
+  double* Bs = dsm + 2 * kDM * kDAS;             // [2][kDK][kDBS]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = warp >> 2, wn = warp & 3;       // 2 x 4 warps of 64 x 32
   const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
-  double acc[8][8];
+  double acc[8][4][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  // global -> register staging: A row (t>>1), k half (t&1)*4; B k-row (t>>5),
-  // columns (t&31)*4
-  float ra[4], rb[4];
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // global -> register staging: A 128 rows x 16 k (8 floats per thread),
+  // B 16 k-rows x 128 cols (8 floats per thread)
+  float ra[8], rb[8];
   auto load = [&](int64_t k0) {
-    const int64_t ar = m0 + (t >> 1), ak = k0 + (t & 1) * 4;
+    const int64_t ar = m0 + (t >> 1), ak = k0 + (t & 1) * 8;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 8; ++q)
       ra[q] = (ar < M && ak + q < K) ? __ldg(A + ar * K + ak + q) : 0.0f;
-    const int64_t bk = k0 + (t >> 5), bn = n0 + (t & 31) * 4;
+    const int64_t bk = k0 + (t >> 4), bn = n0 + (t & 15) * 8;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 8; ++q)
       rb[q] = (bk < K && bn + q < N) ? __ldg(B + bk * N + bn + q) : 0.0f;
   };
   auto stash = [&](int buf) {
+    double* a = As + buf * kDM * kDAS + (t >> 1) * kDAS + (t & 1) * 8;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) As[buf][(t & 1) * 4 + q][t >> 1] = (double)ra[q];
+    for (int q = 0; q < 8; ++q) a[q] = (double)ra[q];
+    double* b = Bs + buf * kDK * kDBS + (t >> 4) * kDBS + (t & 15) * 8;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) Bs[buf][t >> 5][(t & 31) * 4 + q] = (double)rb[q];
+    for (int q = 0; q < 8; ++q) b[q] = (double)rb[q];
   };
   const int64_t nk = (K + kDK - 1) / kDK;
   load(0);
   stash(0);
   __syncthreads();
+  const int fr = lane >> 2, fk = lane & 3;       // fragment row / k of this lane
   for (int64_t kt = 0; kt < nk; ++kt) {
     const int buf = (int)(kt & 1);
     if (kt + 1 < nk) load((kt + 1) * kDK);
-    const int kk_end = (int)min((int64_t)kDK, K - kt * kDK);
-    auto step = [&](int kk) {
-      double a[8], b[8];
-      const double2* ap0 = reinterpret_cast<const double2*>(&As[buf][kk][ty * 4]);
-      const double2* ap1 = reinterpret_cast<const double2*>(&As[buf][kk][64 + ty * 4]);
-      const double2* bp0 = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
-      const double2* bp1 = reinterpret_cast<const double2*>(&Bs[buf][kk][64 + tx * 4]);
-      double2 v;
-      v = ap0[0]; a[0] = v.x; a[1] = v.y;
-      v = ap0[1]; a[2] = v.x; a[3] = v.y;
-      v = ap1[0]; a[4] = v.x; a[5] = v.y;
-      v = ap1[1]; a[6] = v.x; a[7] = v.y;
-      v = bp0[0]; b[0] = v.x; b[1] = v.y;
-      v = bp0[1]; b[2] = v.x; b[3] = v.y;
-      v = bp1[0]; b[4] = v.x; b[5] = v.y;
-      v = bp1[1]; b[6] = v.x; b[7] = v.y;
+    const double* a_s = As + buf * kDM * kDAS + (wm * 64 + fr) * kDAS + fk;
+    const double* b_s = Bs + buf * kDK * kDBS + fk * kDBS + wn * 32 + fr;
+#pragma unroll
+    for (int ks = 0; ks < kDK / 4; ++ks) {       // ascending k, 4 per MMA
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) af[i] = a_s[i * 8 * kDAS + ks * 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = b_s[ks * 4 * kDBS + j * 8];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
-    };
-    if (kk_end == kDK) {
-#pragma unroll
-      for (int kk = 0; kk < kDK; ++kk) step(kk);
-    } else {
-      for (int kk = 0; kk < kk_end; ++kk) step(kk);
+        for (int j = 0; j < 4; ++j)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]) : "d"(af[i]), "d"(bf[j]));
     }
     if (kt + 1 < nk) stash(buf ^ 1);
     __syncthreads();
   }
+  // epilogue: lane holds D[fr][2*fk + {0,1}] of every 8x8 tile
   uint32_t bad = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    const int64_t row = m0 + wm * 64 + i * 8 + fr;
+    if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t col = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      if (row < M && col < N) {
-        const float c = __double2float_rn(acc[i][j]);
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = n0 + wn * 32 + j * 8 + 2 * fk + h;
+        if (col >= N) continue;
+        const float c = __double2float_rn(acc[i][j][h]);
         uint32_t v = 0;
         if (M_ == kStochastic)
           v = variate24(key, (uint64_t)(row_base + row) * (uint64_t)N + (uint64_t)col);
@@ -507,16 +516,22 @@ __global__ void __launch_bounds__(kDT)
     }
   }
   bad = __reduce_or_sync(kFull, bad);
-  if ((t & 31) == 0 && bad) atomicOr(status, kStatusNonFinite);
+  if (lane == 0 && bad) atomicOr(status, kStatusNonFinite);
 }
 
 template <int M_, class Epi>
 void launch_mmq(const float* A, const float* B, float* C, int64_t M, int64_t N,
                 int64_t K, int64_t row_base, const Epi& epi, uint64_t key,
                 uint32_t* status, cudaStream_t s) {
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(k_matmul_q<M_, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDSmem);
+    attr = true;
+  }
   dim3 grid((unsigned)((N + kDN - 1) / kDN), (unsigned)((M + kDM - 1) / kDM));
-  k_matmul_q<M_, Epi><<<grid, kDT, 0, s>>>(A, B, C, M, N, K, row_base, epi, key,
-                                           status);
+  k_matmul_q<M_, Epi><<<grid, kDT, kDSmem, s>>>(A, B, C, M, N, K, row_base, epi,
+                                                key, status);
   note_launch();
 }
 
