@@ -167,3 +167,20 @@ def test_gemm_empty_inner_dimension(q, oracle):
     for fmt in (q.FloatFormat(5, 2), q.FixedFormat(8, 4), q.BlockFloatFormat(8, 0)):
         got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(fmt), 0).cpu().numpy()
         assert np.array_equal(bits(got), np.zeros((5, 7), np.uint32)), fmt
+
+
+@pytest.mark.parametrize("M,N,K", [(131, 77, 1001), (256, 256, 512)])
+def test_matmul_q_adversarial_accumulation(q, oracle, M, N, K):
+    # exponents over 2^-40..2^40 and sign-alternating near-cancelling terms:
+    # any deviation from the ascending-k DFMA chain of the reference
+    # (tensor.cpp:355-376) -- e.g. a reordered or single-rounding k-group sum
+    # in the FP64 tensor-core path -- shows up in the rounded result
+    rng = np.random.default_rng(M * N + K)
+    a = (rng.uniform(1, 2, (M, K)) * 2.0 ** rng.integers(-40, 41, (M, K))
+         * rng.choice([-1, 1], (M, K))).astype(np.float32)
+    b = (rng.uniform(1, 2, (K, N)) * 2.0 ** rng.integers(-40, 41, (K, N))).astype(np.float32)
+    b[1::2] = -b[::2][: b[1::2].shape[0]]  # pairs that nearly cancel
+    c = oracle.matmul(a, b)
+    got = q.quantized_matmul_at(dev(a), dev(b), q.QuantSpec(q.FloatFormat(8, 23)), 0)
+    st, want = oracle.quantize(c, float_fmt(8, 23), NEAREST_EVEN)
+    assert st == 0 and np.array_equal(bits(got.cpu().numpy()), bits(want))
