@@ -427,7 +427,7 @@ struct EpilogueNone {
   __device__ __forceinline__ float apply(float x, uint32_t) const { return x; }
 };
 
-template <int M_, class Epi>
+template <int M_, class Epi, bool VEC>
 __global__ void __launch_bounds__(kDT)
     k_matmul_q(const float* __restrict__ A, const float* __restrict__ B,
                float* __restrict__ C, int64_t M, int64_t N, int64_t K,
@@ -449,13 +449,27 @@ __global__ void __launch_bounds__(kDT)
   float ra[8], rb[8];
   auto load = [&](int64_t k0) {
     const int64_t ar = m0 + (t >> 1), ak = k0 + (t & 1) * 8;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      ra[q] = (ar < M && ak + q < K) ? __ldg(A + ar * K + ak + q) : 0.0f;
     const int64_t bk = k0 + (t >> 4), bn = n0 + (t & 15) * 8;
+    if (VEC && ar < M && ak + 8 <= K) {  // K % 4 == 0, 16-byte aligned rows
+      const float4 u = __ldg(reinterpret_cast<const float4*>(A + ar * K + ak));
+      const float4 w = __ldg(reinterpret_cast<const float4*>(A + ar * K + ak + 4));
+      ra[0] = u.x; ra[1] = u.y; ra[2] = u.z; ra[3] = u.w;
+      ra[4] = w.x; ra[5] = w.y; ra[6] = w.z; ra[7] = w.w;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      rb[q] = (bk < K && bn + q < N) ? __ldg(B + bk * N + bn + q) : 0.0f;
+      for (int q = 0; q < 8; ++q)
+        ra[q] = (ar < M && ak + q < K) ? __ldg(A + ar * K + ak + q) : 0.0f;
+    }
+    if (VEC && bk < K && bn + 8 <= N) {  // N % 4 == 0
+      const float4 u = __ldg(reinterpret_cast<const float4*>(B + bk * N + bn));
+      const float4 w = __ldg(reinterpret_cast<const float4*>(B + bk * N + bn + 4));
+      rb[0] = u.x; rb[1] = u.y; rb[2] = u.z; rb[3] = u.w;
+      rb[4] = w.x; rb[5] = w.y; rb[6] = w.z; rb[7] = w.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        rb[q] = (bk < K && bn + q < N) ? __ldg(B + bk * N + bn + q) : 0.0f;
+    }
   };
   auto stash = [&](int buf) {
     double* a = As + buf * kDM * kDAS + (t >> 1) * kDAS + (t & 1) * 8;
@@ -525,13 +539,20 @@ void launch_mmq(const float* A, const float* B, float* C, int64_t M, int64_t N,
                 uint32_t* status, cudaStream_t s) {
   static bool attr = false;  // per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(k_matmul_q<M_, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kDSmem);
+    cudaFuncSetAttribute(k_matmul_q<M_, Epi, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmem);
+    cudaFuncSetAttribute(k_matmul_q<M_, Epi, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmem);
     attr = true;
   }
   dim3 grid((unsigned)((N + kDN - 1) / kDN), (unsigned)((M + kDM - 1) / kDM));
-  k_matmul_q<M_, Epi><<<grid, kDT, kDSmem, s>>>(A, B, C, M, N, K, row_base, epi,
-                                                key, status);
+  const bool vec = K % 4 == 0 && N % 4 == 0 && aligned16(A) && aligned16(B);
+  if (vec)
+    k_matmul_q<M_, Epi, true><<<grid, kDT, kDSmem, s>>>(A, B, C, M, N, K, row_base,
+                                                        epi, key, status);
+  else
+    k_matmul_q<M_, Epi, false><<<grid, kDT, kDSmem, s>>>(A, B, C, M, N, K, row_base,
+                                                         epi, key, status);
   note_launch();
 }
 
