@@ -290,16 +290,33 @@ __global__ void __launch_bounds__(kSegT)
         const int j = threadIdx.x + k * kSegT;
         if (4 * j < len) v[k] = __ldcs(x4 + j);
       }
-      const bool two = two_factor(sc);
+      // the block-class loops of k_block_rows: two-factor scales, single
+      // factor with / without the stochastic flush guard; float4-shared
+      // variates when the flat indices are 4-aligned (base % 4 == 0)
+      const bool idx4 = (base & 3u) == 0;  // uniform
+      auto run = [&](auto two_t, auto guard_t, auto idx4_t) {
+        constexpr bool TWO = decltype(two_t)::value;
+        constexpr bool GUARD = decltype(guard_t)::value;
+        constexpr bool I4 = decltype(idx4_t)::value;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int j = threadIdx.x + k * kSegT;
-        if (4 * j < len) {
-          bad |= nf4(v[k]);
-          const uint64_t idx = base + (uint64_t)(e0 + 4 * j);
-          __stcs(y4 + j, two ? qb4<M, true, false>(v[k], sc, kmin, kmax, key, idx, rng_mul())
-                             : qb4<M, false, false>(v[k], sc, kmin, kmax, key, idx, rng_mul()));
+        for (int k = 0; k < 4; ++k) {
+          const int j = threadIdx.x + k * kSegT;
+          if (4 * j < len) {
+            bad |= nf4(v[k]);
+            const uint64_t idx = base + (uint64_t)(e0 + 4 * j);
+            __stcs(y4 + j, qb4<M, TWO, I4, GUARD>(v[k], sc, kmin, kmax, key, idx, rng_mul()));
+          }
         }
+      };
+      if (two_factor(sc)) {
+        if (idx4) run(std::true_type{}, std::false_type{}, std::true_type{});
+        else run(std::true_type{}, std::false_type{}, std::false_type{});
+      } else if (M == kStochastic && needs_guard(sc)) {
+        if (idx4) run(std::false_type{}, std::true_type{}, std::true_type{});
+        else run(std::false_type{}, std::true_type{}, std::false_type{});
+      } else {
+        if (idx4) run(std::false_type{}, std::false_type{}, std::true_type{});
+        else run(std::false_type{}, std::false_type{}, std::false_type{});
       }
     } else {
       for (int j = threadIdx.x; j < len; j += kSegT) {
