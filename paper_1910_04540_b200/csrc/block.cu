@@ -153,14 +153,22 @@ __global__ void __launch_bounds__(256)
   if (live) {
     float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
     const uint64_t row_base = base + (uint64_t)(r * L);
+    // block-class loops (see k_block_rows); the class is per row, so it may
+    // differ between the rows of a warp
+    auto run = [&](auto two_t, auto guard_t) {
+      constexpr bool TWO = decltype(two_t)::value;
+      constexpr bool GUARD = decltype(guard_t)::value;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const int64_t j = g + (int64_t)k * G;
-      if (j < L4)
-        __stcs(yr + j, two_factor(sc)
-                           ? qb4<M, true, IDX4>(v[k], sc, kmin, kmax, key, row_base + 4 * j, m32)
-                           : qb4<M, false, IDX4>(v[k], sc, kmin, kmax, key, row_base + 4 * j, m32));
-    }
+      for (int k = 0; k < V; ++k) {
+        const int64_t j = g + (int64_t)k * G;
+        if (j < L4)
+          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(v[k], sc, kmin, kmax, key,
+                                                  row_base + 4 * j, m32));
+      }
+    };
+    if (two_factor(sc)) run(std::true_type{}, std::false_type{});
+    else if (M == kStochastic && needs_guard(sc)) run(std::false_type{}, std::true_type{});
+    else run(std::false_type{}, std::false_type{});
   }
   uint32_t bad = live ? ((sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u)) : 0u;
   bad = __reduce_or_sync(kFull, bad);
