@@ -119,38 +119,50 @@ __global__ void __launch_bounds__(T)
 }
 
 // Short rows (L <= 512 floats): G lanes per row (G a power of two <= 32),
-// V float4 per lane, 32/G rows per warp, 8 warps per CTA; the row maximum is
-// a butterfly over the row's G lanes.  (One CTA per 64-float row would leave
-// most of each CTA idle and make the launch CTA-rate-bound.)
-template <int M, int G, int V, bool IDX4>
+// V float4 per lane, R rows per lane group (their loads all in flight
+// together), 32/G groups per warp, 8 warps per CTA; the row maximum is a
+// butterfly over the row's G lanes.  (One CTA per 64-float row would leave
+// most of each CTA idle and make the launch CTA-rate-bound.)  Iteration i
+// of a warp covers 32/G consecutive rows, so its loads are contiguous.
+template <int M, int G, int V, int R, bool IDX4>
 __global__ void __launch_bounds__(256)
     k_block_rows_small(const float* __restrict__ x, float* __restrict__ y,
                        int64_t L, int64_t nrows, uint64_t base, uint64_t key,
                        int wl, RngMul m32, uint32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r = ((int64_t)blockIdx.x * 8 + warp) * (32 / G) + lane / G;
   const int g = lane % G;
   const int64_t L4 = L >> 2;
-  const bool live = r < nrows;
-  const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
-  float4 v[V];
-  float mf = 0.0f, nf = 0.0f;
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const int64_t j = g + (int64_t)k * G;
-    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live && j < L4) {
-      v[k] = __ldcs(xr + j);
-      absmax_nf(v[k], mf, nf);
-    }
-  }
-  uint32_t m = f2u(mf);
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
-  const BlockScale sc = make_block_scale(m, wl);
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * R * (32 / G) + lane / G;
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
-  if (live) {
+  float4 v[R][V];
+  float nf = 0.0f;
+  uint32_t m[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t r = r0 + (int64_t)i * (32 / G);
+    const float4* __restrict__ xr = reinterpret_cast<const float4*>(x + r * L);
+    float mf = 0.0f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int64_t j = g + (int64_t)k * G;
+      v[i][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nrows && j < L4) {
+        v[i][k] = __ldcs(xr + j);
+        absmax_nf(v[i][k], mf, nf);
+      }
+    }
+    m[i] = f2u(mf);
+  }
+  uint32_t bad = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t r = r0 + (int64_t)i * (32 / G);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) m[i] = max(m[i], __shfl_xor_sync(kFull, m[i], o));
+    if (r >= nrows) continue;
+    const BlockScale sc = make_block_scale(m[i], wl);
+    if (sc.bad) bad |= 2u;
     float4* __restrict__ yr = reinterpret_cast<float4*>(y + r * L);
     const uint64_t row_base = base + (uint64_t)(r * L);
     // block-class loops (see k_block_rows); the class is per row, so it may
@@ -162,7 +174,7 @@ __global__ void __launch_bounds__(256)
       for (int k = 0; k < V; ++k) {
         const int64_t j = g + (int64_t)k * G;
         if (j < L4)
-          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(v[k], sc, kmin, kmax, key,
+          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(v[i][k], sc, kmin, kmax, key,
                                                   row_base + 4 * j, m32));
       }
     };
@@ -170,7 +182,7 @@ __global__ void __launch_bounds__(256)
     else if (M == kStochastic && needs_guard(sc)) run(std::false_type{}, std::true_type{});
     else run(std::false_type{}, std::false_type{});
   }
-  uint32_t bad = live ? ((sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u)) : 0u;
+  if (nf != nf) bad |= 1u;
   bad = __reduce_or_sync(kFull, bad);
   if (lane == 0) flag(status, bad);
 }
@@ -179,13 +191,17 @@ template <int M, int G, int V>
 void launch_rows_small_t(const float* x, float* y, int64_t L, int64_t nrows,
                          uint64_t base, uint64_t key, int wl, uint32_t* st,
                          cudaStream_t s) {
-  const int64_t per_cta = 8 * (32 / G);
+  // several rows per lane group pays for nearest rounding (more loads in
+  // flight: [2^22, 64] 0.365 -> 0.353 ms) but not for stochastic, which is
+  // issue-bound (0.504 -> 0.533 ms)
+  constexpr int R = M == kStochastic ? 1 : (V == 1 ? 4 : (V == 2 ? 2 : 1));
+  const int64_t per_cta = 8 * R * (32 / G);
   const int grid = (int)std::max<int64_t>(
       1, std::min<int64_t>((nrows + per_cta - 1) / per_cta, 0x7FFFFFFF));
   if ((base & 3u) == 0)
-    k_block_rows_small<M, G, V, true><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+    k_block_rows_small<M, G, V, R, true><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   else
-    k_block_rows_small<M, G, V, false><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
+    k_block_rows_small<M, G, V, R, false><<<grid, 256, 0, s>>>(x, y, L, nrows, base, key, wl, rng_mul(), st);
   note_launch();
 }
 
