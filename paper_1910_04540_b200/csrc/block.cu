@@ -226,6 +226,16 @@ void launch_rows(const float* x, float* y, int64_t L, int64_t nrows,
                  uint64_t base, uint64_t key, int wl, uint32_t* st,
                  cudaStream_t s) {
   const int64_t L4 = L >> 2;
+  if (M == kStochastic && L4 <= 64) {
+    // issue-bound: 4 float4 per lane, so the per-row work (butterfly, scale)
+    // is shared by 16 elements per thread rather than 4
+    if (L4 <= 4) launch_rows_small_t<M, 1, 4>(x, y, L, nrows, base, key, wl, st, s);
+    else if (L4 <= 8) launch_rows_small_t<M, 2, 4>(x, y, L, nrows, base, key, wl, st, s);
+    else if (L4 <= 16) launch_rows_small_t<M, 4, 4>(x, y, L, nrows, base, key, wl, st, s);
+    else if (L4 <= 32) launch_rows_small_t<M, 8, 4>(x, y, L, nrows, base, key, wl, st, s);
+    else launch_rows_small_t<M, 16, 4>(x, y, L, nrows, base, key, wl, st, s);
+    return;
+  }
   if (L4 <= 1) launch_rows_small_t<M, 1, 1>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 2) launch_rows_small_t<M, 2, 1>(x, y, L, nrows, base, key, wl, st, s);
   else if (L4 <= 4) launch_rows_small_t<M, 4, 1>(x, y, L, nrows, base, key, wl, st, s);
