@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "block_common.cuh"
 #include "kernels.cuh"
@@ -116,22 +117,29 @@ __global__ void __launch_bounds__(kCT)
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
   const uint64_t ebase = base + (uint64_t)(row * L + s0 * 4);
-  const bool two = two_factor(sc);
-  for (int64_t j0 = threadIdx.x; j0 < len4; j0 += (int64_t)kCT * kU) {
-    float4 v[kU];
+  // block-class loops (see k_block_rows in block.cu)
+  auto run = [&](auto two_t, auto guard_t) {
+    constexpr bool TWO = decltype(two_t)::value;
+    constexpr bool GUARD = decltype(guard_t)::value;
+    for (int64_t j0 = threadIdx.x; j0 < len4; j0 += (int64_t)kCT * kU) {
+      float4 v[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t j = j0 + (int64_t)u * kCT;
-      if (j < len4) v[u] = __ldcs(xr + j);
-    }
+      for (int u = 0; u < kU; ++u) {
+        const int64_t j = j0 + (int64_t)u * kCT;
+        if (j < len4) v[u] = __ldcs(xr + j);
+      }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t j = j0 + (int64_t)u * kCT;
-      if (j < len4)
-        __stcs(yr + j, two ? qb4<M, true, IDX4>(v[u], sc, kmin, kmax, key, ebase + 4 * j, rm)
-                           : qb4<M, false, IDX4>(v[u], sc, kmin, kmax, key, ebase + 4 * j, rm));
+      for (int u = 0; u < kU; ++u) {
+        const int64_t j = j0 + (int64_t)u * kCT;
+        if (j < len4)
+          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(v[u], sc, kmin, kmax, key,
+                                                  ebase + 4 * j, rm));
+      }
     }
-  }
+  };
+  if (two_factor(sc)) run(std::true_type{}, std::false_type{});
+  else if (M == kStochastic && needs_guard(sc)) run(std::false_type{}, std::true_type{});
+  else run(std::false_type{}, std::false_type{});
   uint32_t bad = (sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u);
   bad = __reduce_or_sync(kFull, bad);
   if (lane == 0 && bad) atomicOr(status, bad);
