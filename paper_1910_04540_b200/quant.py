@@ -143,8 +143,15 @@ def _is_device(t) -> bool:
     return torch is not None and isinstance(t, torch.Tensor) and t.is_cuda
 
 
+def _stream_key(device):
+    # status words and workspaces are per (device, stream): calls on
+    # different streams may run concurrently and must not share them
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return idx, torch.cuda.current_stream(idx).cuda_stream
+
+
 def _status_buf(device):
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    key = _stream_key(device)
     buf = _status_bufs.get(key)
     if buf is None:
         buf = torch.zeros(1, dtype=torch.int32, device=device)
@@ -155,7 +162,7 @@ def _status_buf(device):
 def _workspace(device, nbytes):
     if nbytes == 0:
         return None
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    key = _stream_key(device)
     buf = _ws_bufs.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
@@ -177,11 +184,23 @@ def fetch_status(device=None) -> None:
 
 # ---- quantize ----------------------------------------------------------------
 
+def _check_out(out, like):
+    """An `out` tensor is written through a raw pointer: it must be a
+    contiguous fp32 CUDA tensor of the input's element count on its device."""
+    if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32
+            or not out.is_contiguous() or out.device != like.device
+            or out.numel() != like.numel()):
+        raise ValueError("out: a contiguous float32 tensor with the input's "
+                         "element count on the input's device is required")
+
+
 def _quantize_device(t, spec: QuantSpec, call: int, out=None, index_base=0,
                      sync=True):
     if t.dtype != torch.float32:
         raise TypeError("quantize: tensors are fp32 (proj/include/lpsim/tensor.hpp:16)")
     x = t.contiguous()
+    if out is not None:
+        _check_out(out, x)
     y = torch.empty_like(x) if out is None else out
     fmt = spec.format.c()
     shape = shape_array(x.shape)
@@ -351,6 +370,8 @@ def quant_gemm(a, b, fmt_mul: FloatFormat, fmt_add: FloatFormat,
         raise ShapeError("quant_gemm: operands must be rank-2 with matching inner dims")
     M, K = A.shape
     N = B.shape[1]
+    if out is not None:
+        _check_out(out, torch.empty((M, N), dtype=torch.float32, device=dev))
     Cd = torch.empty((M, N), dtype=torch.float32, device=dev) if out is None else out
     nbytes = lib.lpq_quant_gemm_workspace_size(M, N, K)
     ws = _workspace(dev, nbytes)
@@ -391,6 +412,8 @@ def quantized_matmul_at(a, b, spec: QuantSpec, call: int, *, row_base=0,
         raise ShapeError("matmul: operands must be rank-2 with matching inner dims")
     M, K = A.shape
     N = B.shape[1]
+    if out is not None:
+        _check_out(out, torch.empty((M, N), dtype=torch.float32, device=dev))
     Cd = torch.empty((M, N), dtype=torch.float32, device=dev) if out is None else out
     fmt = spec.format.c()
     nbytes = lib.lpq_workspace_size(C.byref(fmt), shape_array((M, N)), 2)

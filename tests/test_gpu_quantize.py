@@ -479,3 +479,31 @@ def test_beyond_2p32_elements_windows(q, oracle):
         assert np.array_equal(bits(yb[r:r + 2].cpu().numpy()), bits(want)), r
     del x, xb, yb
     torch.cuda.empty_cache()
+
+
+def test_out_argument_is_validated(q):
+    x = torch.ones(64, device="cuda")
+    spec = q.QuantSpec(q.FixedFormat(8, 4))
+    for bad in (torch.empty(63, device="cuda"), torch.empty(64, device="cuda", dtype=torch.float16),
+                torch.empty(128, device="cuda")[::2], torch.empty(64)):
+        with pytest.raises(ValueError):
+            q.quantize_fused_at(x, spec, 0, out=bad)
+    out = torch.empty(8, 8, device="cuda")  # same element count, other shape: fine
+    q.quantize_fused_at(x, spec, 0, out=out)
+    assert torch.equal(out.view(-1), torch.ones(64, device="cuda"))
+
+
+def test_concurrent_streams_do_not_share_workspace(q, oracle):
+    # two two-pass block quantizations in flight on two streams at once
+    rng = np.random.default_rng(4)
+    xs = [rng.uniform(-1, 1, (5, 40000)).astype(np.float32) * s for s in (1.0, 1e-3)]
+    spec = q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode.Stochastic, 2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for x, st in zip(xs, (s1, s2)):
+        with torch.cuda.stream(st):
+            outs.append(q.quantize_fused_at(dev(x), spec, 0, sync=False))
+    torch.cuda.synchronize()
+    for x, y in zip(xs, outs):
+        st, want = oracle.quantize(x, block_fmt(8, 0), STOCHASTIC, seed=2, call=0)
+        assert same_bits(y, want)
