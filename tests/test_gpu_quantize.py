@@ -507,3 +507,37 @@ def test_concurrent_streams_do_not_share_workspace(q, oracle):
     for x, y in zip(xs, outs):
         st, want = oracle.quantize(x, block_fmt(8, 0), STOCHASTIC, seed=2, call=0)
         assert same_bits(y, want)
+
+
+@pytest.mark.parametrize("fmt_name", ["fixed", "float", "block0"])
+def test_grouped_index_bases(q, oracle, fmt_name):
+    # lpq_quantize_grouped with per-tensor flat-index bases (aligned and not:
+    # the float4-shared variates need base % 4 == 0) against the oracle
+    import ctypes as C
+    from paper_1910_04540_b200 import _lib
+    fmt, ofmt = {"fixed": (q.FixedFormat(8, 4), fixed_fmt(8, 4)),
+                 "float": (q.FloatFormat(5, 2), float_fmt(5, 2)),
+                 "block0": (q.BlockFloatFormat(8, 0), block_fmt(8, 0))}[fmt_name]
+    rng = np.random.default_rng(8)
+    shapes = [(33, 100), (5000,), (64, 64), (7, 9)]
+    if fmt_name == "block0":
+        shapes = [(33, 100), (50, 8), (64, 64), (7, 12)]
+    bases = [0, 3, 2**33 + 1, 4]
+    xs = [rng.uniform(-3, 3, s).astype(np.float32) for s in shapes]
+    dxs = [dev(x) for x in xs]
+    ys = [torch.empty_like(d) for d in dxs]
+    descs = (_lib.LpqTensorDesc * len(xs))()
+    keep = []
+    for i, (d, y, b) in enumerate(zip(dxs, ys, bases)):
+        shp = _lib.shape_array(d.shape)
+        keep.append(shp)
+        descs[i] = _lib.LpqTensorDesc(d.data_ptr(), y.data_ptr(), shp, d.dim(), 0, b, 10 + i)
+    status = q.quant._status_buf(torch.device("cuda", 0))
+    st = _lib.lib.lpq_quantize_grouped(descs, len(xs), C.byref(fmt.c()), 0, 21, None, 0,
+                                       C.c_void_p(status.data_ptr()),
+                                       q.quant._stream_ptr(torch.device("cuda", 0)))
+    assert st == 0
+    q.fetch_status()
+    for i, (x, y, b) in enumerate(zip(xs, ys, bases)):
+        st, want = oracle.quantize(x, ofmt, STOCHASTIC, seed=21, call=10 + i, index_base=b)
+        assert st == 0 and same_bits(y, want), (fmt_name, i)
