@@ -541,3 +541,18 @@ def test_grouped_index_bases(q, oracle, fmt_name):
     for i, (x, y, b) in enumerate(zip(xs, ys, bases)):
         st, want = oracle.quantize(x, ofmt, STOCHASTIC, seed=21, call=10 + i, index_base=b)
         assert st == 0 and same_bits(y, want), (fmt_name, i)
+
+
+@pytest.mark.parametrize("base", [1, 2, 3, 4, 2**40 + 3])
+def test_index_base_device_path(q, oracle, base):
+    # the variates follow the flat index index_base + i (shard offsets):
+    # every alignment of the base, elementwise and block formats
+    rng = np.random.default_rng(base % 1000)
+    x = rng.uniform(-3, 3, (96, 130)).astype(np.float32)
+    for fmt, ofmt in ((q.FixedFormat(8, 4), fixed_fmt(8, 4)), (q.FloatFormat(5, 2), float_fmt(5, 2)),
+                      (q.BlockFloatFormat(8, 0), block_fmt(8, 0)), (q.BlockFloatFormat(8, 1), block_fmt(8, 1)),
+                      (q.BlockFloatFormat(8), block_fmt(8))):
+        got = q.quantize_fused_at(dev(x), q.QuantSpec(fmt, q.RoundingMode.Stochastic, 6), 2,
+                                  index_base=base)
+        st, want = oracle.quantize(x, ofmt, STOCHASTIC, seed=6, call=2, index_base=base)
+        assert st == 0 and same_bits(got, want), (fmt, base)
