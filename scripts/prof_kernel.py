@@ -21,10 +21,12 @@ specs = {
     "c3": (q.BlockFloatFormat(8, 0), E, 4096), "c3s": (q.BlockFloatFormat(8, 0), S, 4096),
     "whole": (q.BlockFloatFormat(8), E, None), "dim1": (q.BlockFloatFormat(8, 1), E, 64),
     "act": (q.BlockFloatFormat(8, 0), E, 802816),
+    "acts": (q.BlockFloatFormat(8, 0), S, 802816),
+    "short": (q.BlockFloatFormat(8, 0), S, 64),
 }
 fmt, mode, cols = specs[cfg]
 n = 1 << nlog
-if cfg == "act":
+if cfg in ("act", "acts"):
     n = 256 * 802816
 shape = (n // cols, cols) if cols else (n,)
 x = q.random_uniform(shape, 2, 0, -10.0, 10.0)
