@@ -179,6 +179,141 @@ __global__ void __launch_bounds__(kT)
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
 }
 
+// Specialised form for the common slot modes (each slot off, NearestEven or
+// Stochastic -- compile-time), 4 consecutive parameters per thread (float4
+// loads and stores when the tensor's arrays are 16-byte aligned) and the
+// float4-shared variates.  Same per-element semantics as sgd_element.
+constexpr int kOff = -1;
+constexpr int kSgdV = 4;  // parameters per thread (consecutive)
+constexpr int64_t kSgdTileV = (int64_t)kT * kSgdV;
+
+template <int MS>
+__device__ __forceinline__ void quant4(float (&x)[kSgdV], const Slot& s, uint64_t key,
+                                       uint64_t idx, bool idx4, uint32_t& flags) {
+  if (MS == kOff) return;
+  uint32_t v[kSgdV] = {0u, 0u, 0u, 0u};
+  if (MS == kStochastic) {
+    if (idx4) {
+      variate24_x4(key, idx, 32u, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSgdV; ++q) v[q] = variate24(key, idx + q);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kSgdV; ++q) {
+    if (nonfinite(x[q])) flags |= kStatusNonFinite;
+    x[q] = q_mode<MS == kOff ? kNearestEven : MS>(x[q], s, v[q]);
+  }
+}
+
+template <int MG, int MA, int MW>
+__global__ void __launch_bounds__(kT)
+    k_sgd_grouped_t(const __grid_constant__ SgdTable t, float momentum, float lr,
+                    uint32_t* __restrict__ status) {
+  int lo = 0, hi = t.count - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.e[mid].first <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const SgdEntry& e = t.e[lo];
+  const int64_t i0 = ((int64_t)blockIdx.x - e.first) * kSgdTileV + (int64_t)threadIdx.x * kSgdV;
+  if (i0 >= e.n) return;
+  const bool vec = i0 + kSgdV <= e.n &&
+      ((reinterpret_cast<uintptr_t>(e.g) | reinterpret_cast<uintptr_t>(e.v) |
+        reinterpret_cast<uintptr_t>(e.a) | reinterpret_cast<uintptr_t>(e.w)) & 15u) == 0;
+  const int cnt = (int)min((int64_t)kSgdV, e.n - i0);
+  float g[kSgdV], v[kSgdV], a[kSgdV];
+  if (vec) {
+    const float4 g4 = __ldcs(reinterpret_cast<const float4*>(e.g + i0));
+    const float4 v4 = __ldcs(reinterpret_cast<const float4*>(e.v + i0));
+    const float4 a4 = __ldcs(reinterpret_cast<const float4*>(e.a + i0));
+    g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
+    v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+    a[0] = a4.x; a[1] = a4.y; a[2] = a4.z; a[3] = a4.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kSgdV; ++q) {
+      g[q] = q < cnt ? e.g[i0 + q] : 0.0f;
+      v[q] = q < cnt ? e.v[i0 + q] : 0.0f;
+      a[q] = q < cnt ? e.a[i0 + q] : 0.0f;
+    }
+  }
+  const uint64_t idx = e.base + (uint64_t)i0;
+  const bool idx4 = (idx & 3u) == 0;
+  uint32_t flags = 0;
+  quant4<MG>(g, t.q[0], e.key[0], idx, idx4, flags);         // g = Qg(grad)
+#pragma unroll
+  for (int q = 0; q < kSgdV; ++q) {
+    v[q] = __fadd_rn(__fmul_rn(momentum, v[q]), g[q]);      // add(scale(vel, m), g)
+    if (q < cnt && nonfinite(v[q])) flags |= kStatusInvalidValue;
+  }
+  quant4<MA>(v, t.q[1], e.key[1], idx, idx4, flags);         // vel = Qa(v)
+  float w[kSgdV];
+#pragma unroll
+  for (int q = 0; q < kSgdV; ++q) {
+    const float lv = __fmul_rn(v[q], lr);                   // scale(v, lr)
+    a[q] = __fsub_rn(a[q], lv);                             // sub(acc, .)
+    if (q < cnt && (nonfinite(lv) || nonfinite(a[q]))) flags |= kStatusInvalidValue;
+  }
+  quant4<MA>(a, t.q[2], e.key[2], idx, idx4, flags);         // acc = Qa(a)
+#pragma unroll
+  for (int q = 0; q < kSgdV; ++q) w[q] = a[q];
+  quant4<MW>(w, t.q[3], e.key[3], idx, idx4, flags);         // w = Qw(acc)
+  if (vec) {
+    __stcs(reinterpret_cast<float4*>(e.v + i0), make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<float4*>(e.a + i0), make_float4(a[0], a[1], a[2], a[3]));
+    __stcs(reinterpret_cast<float4*>(e.w + i0), make_float4(w[0], w[1], w[2], w[3]));
+  } else {
+#pragma unroll
+    for (int q = 0; q < kSgdV; ++q)
+      if (q < cnt) {
+        e.v[i0 + q] = v[q];
+        e.a[i0 + q] = a[q];
+        e.w[i0 + q] = w[q];
+      }
+  }
+  // (padding lanes q >= cnt hold zeros: finite, results discarded)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if (flags) atomicOr(status, flags);
+}
+
+// slot mode as a template value: kOff, NearestEven, Stochastic; -2 = other
+__host__ inline int fast_mode(const Slot& s) {
+  if (!s.enabled) return kOff;
+  if (s.mode == kNearestEven || s.mode == kStochastic) return s.mode;
+  return -2;
+}
+
+template <int MG, int MA>
+cudaError_t launch_sgd_w(int mw, const SgdTable& t, float m, float lr,
+                         uint32_t* st, cudaStream_t s) {
+  const unsigned grid = (unsigned)t.ctas;
+  switch (mw) {
+    case kOff: k_sgd_grouped_t<MG, MA, kOff><<<grid, kT, 0, s>>>(t, m, lr, st); break;
+    case kNearestEven: k_sgd_grouped_t<MG, MA, kNearestEven><<<grid, kT, 0, s>>>(t, m, lr, st); break;
+    default: k_sgd_grouped_t<MG, MA, kStochastic><<<grid, kT, 0, s>>>(t, m, lr, st); break;
+  }
+  return cudaGetLastError();
+}
+template <int MG>
+cudaError_t launch_sgd_a(int ma, int mw, const SgdTable& t, float m, float lr,
+                         uint32_t* st, cudaStream_t s) {
+  switch (ma) {
+    case kOff: return launch_sgd_w<MG, kOff>(mw, t, m, lr, st, s);
+    case kNearestEven: return launch_sgd_w<MG, kNearestEven>(mw, t, m, lr, st, s);
+    default: return launch_sgd_w<MG, kStochastic>(mw, t, m, lr, st, s);
+  }
+}
+cudaError_t launch_sgd_fast(int mg, int ma, int mw, const SgdTable& t, float m,
+                            float lr, uint32_t* st, cudaStream_t s) {
+  switch (mg) {
+    case kOff: return launch_sgd_a<kOff>(ma, mw, t, m, lr, st, s);
+    case kNearestEven: return launch_sgd_a<kNearestEven>(ma, mw, t, m, lr, st, s);
+    default: return launch_sgd_a<kStochastic>(ma, mw, t, m, lr, st, s);
+  }
+}
+
 lpq_status make_slot(const lpq_quant_slot* in, Slot* out) {
   *out = Slot{};
   if (!in || !in->enabled) return LPQ_OK;
@@ -254,14 +389,25 @@ extern "C" lpq_status lpq_sgd_step_grouped(const lpq_sgd_tensor* tensors,
   }
   if (!d_status) return LPQ_ERR_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the two accumulator slots share the spec; both must match for the
+  // specialised kernel
+  const int mg = fast_mode(t.q[0]), ma = fast_mode(t.q[1]), mw = fast_mode(t.q[3]);
+  const bool fast = mg != -2 && ma != -2 && mw != -2 && fast_mode(t.q[2]) == ma;
+  const int64_t tile = fast ? kSgdTileV : kSgdTile;
   auto flush = [&]() -> cudaError_t {
     if (t.count == 0) return cudaSuccess;
-    k_sgd_grouped<<<(unsigned)t.ctas, kT, 0, s>>>(t, momentum, lr, d_status);
+    cudaError_t e;
+    if (fast) {
+      e = launch_sgd_fast(mg, ma, mw, t, momentum, lr, d_status, s);
+    } else {
+      k_sgd_grouped<<<(unsigned)t.ctas, kT, 0, s>>>(t, momentum, lr, d_status);
+      e = cudaGetLastError();
+    }
     note_launch();
     note_passes(1);
     t.count = 0;
     t.ctas = 0;
-    return cudaGetLastError();
+    return e;
   };
   for (int i = 0; i < count; ++i) {
     const lpq_sgd_tensor& d = tensors[i];
@@ -281,7 +427,7 @@ extern "C" lpq_status lpq_sgd_step_grouped(const lpq_sgd_tensor* tensors,
     for (int k = 0; k < 4; ++k)
       e.key[k] = t.q[k].enabled ? stream_key(in[k]->seed, calls[k]) : 0u;
     e.first = t.ctas;
-    t.ctas += (d.n + kSgdTile - 1) / kSgdTile;
+    t.ctas += (d.n + tile - 1) / tile;
   }
   const cudaError_t e = flush();
   return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
