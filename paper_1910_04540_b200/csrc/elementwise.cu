@@ -22,7 +22,12 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnrollBig = 8;    // 8 float4 = 128 B in flight per thread
-constexpr int kUnrollSmall = 4;  // tensors below 2^26 elements: finer tail
+// tensors below 2^26 elements: a finer last wave (graph-captured
+// back-to-back 2^24 launches, scripts/time_b2b.py: nearest best at 4 float4
+// per thread, stochastic at 6 -- float(5,2) 4869 -> 4969 GB/s, fixed(8,4)
+// 5683 -> 5874)
+template <int M>
+constexpr int unroll_small() { return M == kStochastic ? 6 : 4; }
 
 template <bool TINY>
 struct FixedSatOp {
@@ -172,10 +177,11 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   // retire and launch in address order, which keeps the DRAM pages in use
   // compact.  Measured on B200 (scripts/ew_variants.cu, 2^30 elements):
   // persistent grid-stride 5.85 TB/s vs one-trip 8 x float4 6.59 TB/s.
-  // tensors below 2^26 elements: 4 float4 per thread, a finer last wave
-  // (graph-captured back-to-back launches, scripts/time_b2b.py: 2^24
-  // float(5,2) nearest 6082 -> 6319 GB/s, 2^20 stochastic 1764 -> 2032)
+  // tensors below 2^26 elements: fewer float4 per thread (unroll_small), a
+  // finer last wave (2^24 float(5,2) nearest 6082 -> 6319 GB/s with 4, 2^20
+  // stochastic 1764 -> 2032)
   const bool small = idx4 && n < (int64_t(1) << 26);
+  constexpr int kUnrollSmall = unroll_small<M>();
   const int unroll = small ? kUnrollSmall : kUnrollBig;
   const int64_t want = (work + (int64_t)kThreads * unroll - 1) /
                        ((int64_t)kThreads * unroll);
