@@ -166,6 +166,16 @@ def cpu_reference_time(fmt_c, mode, xs, shape, threads, repeats):
     return statistics.median(times)
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -417,11 +427,17 @@ def run_ours(args, rank, world, local_rank):
             th = cpu_threads()
             secs = cpu_reference_time(oracle_fmt(cfg), mode_id(cfg), xh, samp_shape,
                                       th, args.cpu_repeats)
+            # one thread too, on a quarter of the sample
+            s1 = samp // 4 if cfg["kind"] != "block" else (samp // 4 // cfg["cols"]) * cfg["cols"]
+            s1_shape = (s1 // cfg["cols"], cfg["cols"]) if cfg["kind"] == "block" else (s1,)
+            secs1 = cpu_reference_time(oracle_fmt(cfg), mode_id(cfg), xh[:s1], s1_shape, 1, 1)
             cpu = {"value": round(8 * samp / secs / 1e9, 4), "unit": "GB/s",
                    "cores": th, "kind": "reference",
                    "sample": f"first {samp} elements of this workload's input, "
                              f"lpsim::quantize_fused_at (oracle/_ref, -O3), "
-                             f"set_num_threads({th}), median of {args.cpu_repeats}"}
+                             f"set_num_threads({th}), median of {args.cpu_repeats}",
+                   "value_1thread": round(8 * s1 / secs1 / 1e9, 4),
+                   "cpu_model": cpu_model()}
         except Exception as e:  # the baseline must not sink the GPU line
             cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {e}"}
