@@ -32,6 +32,9 @@ constexpr int unroll_small() { return M == kStochastic ? 6 : 4; }
 template <bool TINY>
 struct FixedSatOp {
   static constexpr bool kFmaRng = false;  // FMA-pipe-bound already
+  static constexpr bool kBits = false;
+  template <int M>
+  __device__ __forceinline__ float4 apply4(const float4& x, const uint32_t (&)[4]) const { return x; }
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
@@ -41,6 +44,9 @@ struct FixedSatOp {
 };
 struct FixedWrapOp {
   static constexpr bool kFmaRng = true;
+  static constexpr bool kBits = false;
+  template <int M>
+  __device__ __forceinline__ float4 apply4(const float4& x, const uint32_t (&)[4]) const { return x; }
   FixedParams p;
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
@@ -52,7 +58,26 @@ struct FixedWrapOp {
 template <int V>
 struct FloatOp {
   static constexpr bool kFmaRng = V != 2;  // the scaled form is FMA-heavy
+  static constexpr bool kBits = V != 0;   // apply4: the bit-domain form
   FloatParams p;
+  // Four elements: the bit-domain form when every element is zero or in the
+  // normal range of the format (the common case), else the per-element form.
+  template <int M>
+  __device__ __forceinline__ float4 apply4(const float4& x, const uint32_t (&v)[4]) const {
+    constexpr int MF = M == kNearestEven ? kNearestEven : kStochastic;
+    const float c[4] = {fminf(fmaxf(x.x, -p.max_value), p.max_value),
+                        fminf(fmaxf(x.y, -p.max_value), p.max_value),
+                        fminf(fmaxf(x.z, -p.max_value), p.max_value),
+                        fminf(fmaxf(x.w, -p.max_value), p.max_value)};
+    bool under = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) under |= fabsf(c[q]) < p.min_normal && c[q] != 0.0f;
+    if (!under && p.bits_ok)
+      return make_float4(quant_float_bits<MF>(c[0], p, v[0]), quant_float_bits<MF>(c[1], p, v[1]),
+                         quant_float_bits<MF>(c[2], p, v[2]), quant_float_bits<MF>(c[3], p, v[3]));
+    return make_float4(apply<M>(x.x, v[0]), apply<M>(x.y, v[1]), apply<M>(x.z, v[2]),
+                       apply<M>(x.w, v[3]));
+  }
   template <int M>
   __device__ __forceinline__ float apply(float x, uint32_t v) const {
     constexpr int MF = M == kNearestEven ? kNearestEven : kStochastic;
@@ -90,7 +115,9 @@ __device__ __forceinline__ float qelem_v(const Op& op, float x, uint32_t v,
 // IDX4: (base + head) % 4 == 0, so the four flat indices of a float4 differ
 // from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
 template <int M, class Op, bool IDX4, int kUnroll>
-__global__ void __launch_bounds__(kThreads)
+// (float ops with the bit-domain form: <= 64 registers, 4 CTAs per SM --
+// the inlined fallback path would otherwise cost one CTA per SM)
+__global__ void __launch_bounds__(kThreads, Op::kBits ? 4 : 0)
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
                   RngMul rm, uint32_t* __restrict__ status) {
@@ -112,6 +139,16 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t j = i0 + (int64_t)u * kThreads;
       if (j < n4) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
+        if (Op::kBits && (M == kNearestEven || (M == kStochastic && IDX4))) {
+          uint32_t vv[4] = {0u, 0u, 0u, 0u};
+          if (M == kStochastic) variate24_x4(key, idx, rm.m32, vv);
+          nf = __fmaf_rn(v[u].x, 0.0f, nf);
+          nf = __fmaf_rn(v[u].y, 0.0f, nf);
+          nf = __fmaf_rn(v[u].z, 0.0f, nf);
+          nf = __fmaf_rn(v[u].w, 0.0f, nf);
+          __stcs(y4 + j, op.template apply4<M>(v[u], vv));
+          continue;
+        }
         if (M == kStochastic && IDX4) {  // the float4's variates together
           uint32_t vv[4];
           variate24_x4(key, idx, rm.m32, vv);

@@ -471,6 +471,15 @@ struct FloatParams {
   uint32_t m_sh9;    // 2^9   (runtime multipliers, see RngMul)
   uint32_t m_two;    // 2
   uint32_t m_sh8;    // 2^8
+  // bit-domain form (quant_float_bits): |x| >= 2^min_exp or x == 0
+  int32_t bits_ok;   // man <= 22
+  uint32_t rmask;    // the 23 - man mantissa bits that are rounded off
+  uint32_t rhalf;    // rmask >> 1 (RNE: half the step, minus one ulp)
+  uint32_t rshift;   // 23 - man (RNE: the kept LSB = the parity of k)
+  uint32_t rodd;     // 1; 0 for man == 0, where k = 1 is always odd (rhalf
+                     // then carries the +1: ties round up to k = 2)
+  uint32_t vshift;   // 1 + man (stochastic: R = (~v & 0xFFFFFF) >> vshift)
+  float min_normal;  // 2^min_exp
   uint32_t m_neg23;  // -2^23 (mod 2^32)
   uint32_t m_pos23;  // 2^23
   uint32_t sc_bits;  // (254 + man) << 23
@@ -504,6 +513,13 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.m_pos23 = 1u << 23;
   p.sc_bits = (uint32_t)(254 + man_bits) << 23;
   p.inv_bits = 0u - ((uint32_t)man_bits << 23);
+  p.bits_ok = man_bits <= 22 ? 1 : 0;
+  p.rmask = man_bits <= 22 ? (1u << (23 - man_bits)) - 1u : 0u;
+  p.rhalf = (p.rmask >> 1) + (man_bits == 0 ? 1u : 0u);
+  p.rodd = man_bits == 0 ? 0u : 1u;
+  p.rshift = man_bits <= 22 ? (uint32_t)(23 - man_bits) : 0u;
+  p.vshift = (uint32_t)(1 + man_bits);
+  p.min_normal = p.min_exp >= -126 ? u2f((uint32_t)(127 + p.min_exp) << 23) : 0.0f;
   return p;
 }
 
@@ -580,6 +596,41 @@ LPQ_HD float quant_float_scaled(float x, const FloatParams& p, uint32_t v) {
   const float k = round_signed<M>(fmul(xc, sc), v);
   const float q = fma_rn(k, inv, 0.0f);
   return x == 0.0f ? x : q;
+}
+
+// Float quantizer in the bit domain for |x| >= 2^min_exp (and x == +-0),
+// NearestEven / Stochastic, man <= 22, x already clamped to +-max_value.
+// In that range the grid is x's own binade with man fraction bits, so the
+// rounding is integer arithmetic on the IEEE bits: add to the magnitude and
+// clear the 23 - man dropped bits (a carry out of the mantissa steps to the
+// next binade exactly as k = 2^(man+1) does; max_value is on the grid, so no
+// clamped value rounds past it; +-0 stay +-0 as the reference returns x).
+//  * NearestEven: + (half step - 1 ulp) + the kept LSB (ties to even).
+//  * Stochastic: the reference rounds the SIGNED r = x * 2^(man-E) up
+//    (toward +inf) iff u < r - floor(r), u = v * 2^-24.  With L the dropped
+//    bits of |x| and s = 23 - man, frac|r| = L * 2^-s, so the magnitude goes
+//    up iff  x > 0: v < L * 2^(1+man)    x < 0: v >= 2^24 - L * 2^(1+man).
+//    Adding R to the magnitude and truncating carries iff L + R >= 2^s:
+//    x > 0: R = (2^24 - 1 - v) >> (1+man):  L + R >= 2^s <=> v < L * 2^(1+man)
+//    x < 0: R = v >> (1+man):               L + R >= 2^s <=> v >= 2^24 - L * 2^(1+man)
+//    (all integers) -- the same decision, bit for bit.
+// Values below 2^min_exp (the two-point underflow grid) take
+// quant_float_scaled.  Identical results to quant_float<M>.
+template <int M>
+LPQ_HD float quant_float_bits(float xc, const FloatParams& p, uint32_t v) {
+  uint32_t b = f2u(xc);
+  if (M == kStochastic) {
+#if defined(__CUDA_ARCH__)
+    uint32_t neg;  // all ones iff x < 0 (one SHF.R.S32)
+    asm("shr.s32 %0, %1, 31;" : "=r"(neg) : "r"(b));
+#else
+    const uint32_t neg = (uint32_t)((int32_t)b >> 31);
+#endif
+    b += (v ^ (~neg & 0xFFFFFFu)) >> p.vshift;
+  } else {
+    b += p.rhalf + ((b >> p.rshift) & p.rodd);
+  }
+  return u2f(b & ~p.rmask);
 }
 
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;

@@ -3,6 +3,7 @@
 // TEST INFRASTRUCTURE ONLY: not part of the product library; exists so the
 // exact source the sm_100a kernels inline can be swept over millions of
 // inputs on a machine without a GPU.
+#include <math.h>
 #include <stdint.h>
 
 #include "../../paper_1910_04540_b200/csrc/quant_math.cuh"
@@ -16,7 +17,21 @@ void run(const float* x, const uint32_t* v, float* y, int64_t n, const Fmt* f) {
     // the kernels' dispatch: the streaming form for even/stochastic unless
     // |x| * 2^-min_exp can flush to zero
     const lpq::FloatParams p = lpq::make_float(f->exp_bits, f->man_bits);
-    if ((M == 0 || M == 1) && p.scaled_ok)
+    // the bit-domain form wherever the kernels may take it (zero or the
+    // normal range of the format, after the clamp), the streaming forms
+    // elsewhere
+    if ((M == 0 || M == 1) && (p.scaled_ok || !p.tiny) && p.bits_ok) {
+      for (int64_t i = 0; i < n; ++i) {
+        const float xc = fminf(fmaxf(x[i], -p.max_value), p.max_value);
+        const uint32_t vi = v ? v[i] : 0u;
+        if (!(fabsf(xc) < p.min_normal && xc != 0.0f))
+          y[i] = lpq::quant_float_bits<(M == 0 ? 0 : 1)>(xc, p, vi);
+        else if (p.scaled_ok)
+          y[i] = lpq::quant_float_scaled<(M == 0 ? 0 : 1)>(x[i], p, vi);
+        else
+          y[i] = lpq::quant_float_fast<(M == 0 ? 0 : 1)>(x[i], p, vi);
+      }
+    } else if ((M == 0 || M == 1) && p.scaled_ok)
       for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float_scaled<(M == 0 ? 0 : 1)>(x[i], p, v ? v[i] : 0u);
     else if ((M == 0 || M == 1) && !p.tiny)
       for (int64_t i = 0; i < n; ++i) y[i] = lpq::quant_float_fast<(M == 0 ? 0 : 1)>(x[i], p, v ? v[i] : 0u);
