@@ -116,8 +116,9 @@ __device__ __forceinline__ float qelem_v(const Op& op, float x, uint32_t v,
 // from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
 template <int M, class Op, bool IDX4, int kUnroll>
 // (float ops with the bit-domain form: <= 64 registers, 4 CTAs per SM --
-// the inlined fallback path would otherwise cost one CTA per SM)
-__global__ void __launch_bounds__(kThreads, Op::kBits ? 4 : 0)
+// the inlined fallback path would otherwise cost one CTA per SM; 5 for the
+// small-tensor nearest kernel: C1 nearest 5971 -> 6096 GB/s)
+__global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M == kStochastic ? 4 : 5))
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
                   RngMul rm, uint32_t* __restrict__ status) {
