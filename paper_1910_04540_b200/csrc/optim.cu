@@ -47,6 +47,13 @@ template <int M>
 __device__ __forceinline__ float q_mode(float x, const Slot& s, uint32_t v) {
   constexpr bool kFast = M == kNearestEven || M == kStochastic;
   if (s.kind == LPQ_FLOAT) {
+    constexpr int MF = kFast ? M : kNearestEven;
+    if (kFast && s.fp.bits_ok && (s.fp.scaled_ok || !s.fp.tiny)) {
+      // the bit-domain form for zero and the normal range (quant_float_bits)
+      const float xc = fminf(fmaxf(x, -s.fp.max_value), s.fp.max_value);
+      if (!(fabsf(xc) < s.fp.min_normal && xc != 0.0f))
+        return quant_float_bits<MF>(xc, s.fp, v);
+    }
     if (kFast && s.fp.scaled_ok) return quant_float_scaled<kFast ? M : kNearestEven>(x, s.fp, v);
     if (kFast && !s.fp.tiny) return quant_float_fast<kFast ? M : kNearestEven>(x, s.fp, v);
     return quant_float<M>(x, s.fp, v);
