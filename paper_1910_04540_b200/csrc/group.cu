@@ -75,8 +75,7 @@ struct FltOp {
   template <int M> __device__ __forceinline__ float apply(float x, uint32_t v) const {
     constexpr bool kFast = M == kNearestEven || M == kStochastic;
     constexpr int MF = kFast ? M : kNearestEven;
-    if (kFast && p.scaled_ok) return quant_float_scaled<MF>(x, p, v);
-    if (kFast && !p.tiny) return quant_float_fast<MF>(x, p, v);
+    if (kFast) return quant_float_stream<MF>(x, p, v);
     return quant_float<M>(x, p, v);
   }
 };

@@ -633,6 +633,20 @@ LPQ_HD float quant_float_bits(float xc, const FloatParams& p, uint32_t v) {
   return u2f(b & ~p.rmask);
 }
 
+// One element, NearestEven / Stochastic, any float format: the bit-domain
+// form for zero and the normal range, else the streaming forms (identical
+// results to quant_float<M>).
+template <int M>
+LPQ_HD float quant_float_stream(float x, const FloatParams& p, uint32_t v) {
+  if (p.bits_ok && (p.scaled_ok || !p.tiny)) {
+    const float xc = fminf(fmaxf(x, -p.max_value), p.max_value);
+    if (!(fabsf(xc) < p.min_normal && xc != 0.0f)) return quant_float_bits<M>(xc, p, v);
+  }
+  if (p.scaled_ok) return quant_float_scaled<M>(x, p, v);
+  if (!p.tiny) return quant_float_fast<M>(x, p, v);
+  return quant_float<M>(x, p, v);
+}
+
 // ---- block floating point (block_quant_one_m, scalar_quant.hpp:80-87;
 //      fused_block, quant_ops.cpp:68-115) ------------------------------------
 
