@@ -380,13 +380,19 @@ def run_ours(args, rank, world, local_rank):
                 ct.append(time.perf_counter() - t0)
             ceiling = round(bytes_per_rank_step / min(ct) / 1e9, 3)
             del dtmp
+        b_in, b_out = C.c_int(), C.c_int()
+        _lib.lib.lpq_host_bytes_per_element(C.byref(fmt_c), int(spec.mode), C.byref(b_in),
+                                            C.byref(b_out))
         e2e = {"value": round(bytes_per_rank_step * world * e_steps / et / 1e9, 3),
-               "unit": "GB/s", "h2d_bytes_per_step": 4 * n * world,
-               "d2h_bytes_per_step": 4 * n * world, "steps": e_steps,
+               "unit": "GB/s", "h2d_bytes_per_step": b_in.value * n * world,
+               "d2h_bytes_per_step": b_out.value * n * world, "steps": e_steps,
                "api": f"lpq_quantize_host (include/lpq.h), {host_mem} host buffers",
                "pcie_copy_ceiling": ceiling,
-               "pcie_copy_ceiling_note": "per GPU: concurrent bare H2D(input)+D2H(output) copies "
-                                         "of the same pinned buffers, metric units"}
+               "pcie_copy_ceiling_note": "per GPU: concurrent bare H2D(input)+D2H(output) fp32 "
+                                         "copies of the same pinned buffers, metric units",
+               "d2h_format": ("one-byte codes of the quantized values, decoded on the host "
+                              "(bit-identical; include/lpq.h)" if b_out.value == 1
+                              else "fp32")}
         del hx, hy
     # ---- roofline of the dominant kernel --------------------------------------------
     peak, peak_src, peaks = load_peaks()

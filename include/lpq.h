@@ -249,11 +249,18 @@ lpq_status lpq_sgd_step_grouped(const lpq_sgd_tensor* tensors, int count,
 /* ---- host entry points (synchronous; host buffers) ---------------------- */
 
 /* quantize_fused_at over host memory on CUDA device `device` (-1 = current):
- * H2D, kernels and D2H are pipelined in chunks. */
+ * H2D, kernels and D2H are pipelined in chunks.  For saturating fixed point
+ * with wl <= 8 and float formats with 1 + exp + man <= 8 (NearestEven /
+ * Stochastic) the device->host copy carries one-byte codes of the quantized
+ * values, decoded on the host through a 256-entry table (bit-identical). */
 lpq_status lpq_quantize_host(const float* x, float* y, const int64_t* shape,
                              int rank, uint64_t index_base,
                              const lpq_format* f, int mode, uint64_t seed,
                              uint64_t call, int device);
+
+/* Bytes per element lpq_quantize_host moves host->device and device->host
+ * for this format and mode (4 and 4, or 4 and 1 with byte codes). */
+void lpq_host_bytes_per_element(const lpq_format* f, int mode, int* h2d, int* d2h);
 
 lpq_status lpq_quantize_composed_host(const float* x, float* y,
                                       const int64_t* shape, int rank,

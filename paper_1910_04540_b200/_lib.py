@@ -140,6 +140,7 @@ _PROTOS = {
     "lpq_quantize_grouped": (C.c_int, [C.POINTER(LpqTensorDesc), C.c_int, _F,
                                        C.c_int, C.c_uint64, _VP, C.c_size_t,
                                        _VP, _VP]),
+    "lpq_host_bytes_per_element": (None, [_F, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "lpq_parse_format": (C.c_int, [C.c_char_p, _F]),
     "lpq_parse_rounding": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
     "lpq_format_to_string": (C.c_int, [_F, C.c_char_p, C.c_size_t]),

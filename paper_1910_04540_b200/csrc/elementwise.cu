@@ -249,6 +249,39 @@ cudaError_t dispatch_mode(const float* x, float* y, int64_t n, uint64_t base,
   }
 }
 
+// ---- byte codes of quantized values (host-path device->host copy) -----------
+
+__device__ __forceinline__ uint8_t encode8(float q, const ByteCode& bc) {
+  if (bc.kind == 1) return (uint8_t)__float2int_rn(__fmul_rn(q, bc.scale));  // exact k
+  const uint32_t b = f2u(q);
+  const uint32_t sign = (b >> 31) << 7;
+  const uint32_t ab = b & 0x7FFFFFFFu;
+  if (ab == 0u) return (uint8_t)sign;
+  const int e = (int)(ab >> 23) - 127;  // quantized values are normal
+  const uint32_t ei = (uint32_t)(e - bc.min_exp + 1);
+  const uint32_t mt = (ab >> (23 - bc.man)) & ((1u << bc.man) - 1u);
+  return (uint8_t)(sign | (ei << bc.man) | mt);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_encode8(const float* __restrict__ q, uint8_t* __restrict__ c, int64_t n,
+              ByteCode bc) {
+  const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * 16;
+  if (i0 + 16 <= n && (reinterpret_cast<uintptr_t>(q + i0) & 15u) == 0 &&
+      (reinterpret_cast<uintptr_t>(c + i0) & 15u) == 0) {
+    uint32_t w[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(q + i0) + g);
+      w[g] = (uint32_t)encode8(v.x, bc) | ((uint32_t)encode8(v.y, bc) << 8) |
+             ((uint32_t)encode8(v.z, bc) << 16) | ((uint32_t)encode8(v.w, bc) << 24);
+    }
+    __stcs(reinterpret_cast<uint4*>(c + i0), make_uint4(w[0], w[1], w[2], w[3]));
+  } else {
+    for (int64_t i = i0; i < n && i < i0 + 16; ++i) c[i] = encode8(q[i], bc);
+  }
+}
+
 // ---- generators -------------------------------------------------------------
 
 __global__ void __launch_bounds__(kThreads)
@@ -295,6 +328,15 @@ cudaError_t launch_float(const float* x, float* y, int64_t n, uint64_t base,
   if (!p.tiny)
     return dispatch_mode(x, y, n, base, key, FloatOp<1>{p}, mode, status, s);
   return dispatch_mode(x, y, n, base, key, FloatOp<0>{p}, mode, status, s);
+}
+
+cudaError_t launch_encode8(const float* q, uint8_t* c, int64_t n, const ByteCode& bc,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t per = (int64_t)kThreads * 16;
+  k_encode8<<<(unsigned)((n + per - 1) / per), kThreads, 0, s>>>(q, c, n, bc);
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,

@@ -67,6 +67,17 @@ cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
                                 uint32_t* maxima, cudaStream_t s);
 
 // ---- generators -------------------------------------------------------------
+// One-byte codes of quantized values for the host path's device->host copy
+// (runtime.cu): see ByteCode.  q: quantized fp32 values (device), c: codes.
+struct ByteCode {
+  int32_t kind;     // 0: none, 1: fixed (k = q * 2^fl), 2: float (sign|E|man)
+  float scale;      // fixed: 2^fl
+  int32_t man;      // float: mantissa bits kept
+  int32_t min_exp;  // float: exponent of code E = 1
+};
+cudaError_t launch_encode8(const float* q, uint8_t* c, int64_t n, const ByteCode& bc,
+                           cudaStream_t s);
+
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,
                            float lo, float hi, cudaStream_t s);
 cudaError_t launch_variates(float* y, int64_t n, uint64_t base, uint64_t key,

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <condition_variable>
 #include <cstring>
 #include <memory>
@@ -39,6 +40,8 @@ struct HostCtx {
   float* dbuf[kStreams] = {};
   float* pin_in[kStreams] = {};
   float* pin_out[kStreams] = {};
+  uint8_t* dcode[kStreams] = {};   // device byte codes of a chunk
+  uint8_t* pcode[kStreams] = {};   // page-locked byte codes of a chunk
   int64_t chunk_cap = 0;  // elements per chunk buffer
   uint32_t* d_status = nullptr;
   void* ws = nullptr;
@@ -55,6 +58,10 @@ struct HostCtx {
       if (dbuf[k]) cudaFree(dbuf[k]);
       if (pin_in[k]) cudaFreeHost(pin_in[k]);
       if (pin_out[k]) cudaFreeHost(pin_out[k]);
+      if (dcode[k]) cudaFree(dcode[k]);
+      if (pcode[k]) cudaFreeHost(pcode[k]);
+      dcode[k] = nullptr;
+      pcode[k] = nullptr;
       if (done[k]) cudaEventDestroy(done[k]);
       if (st[k]) cudaStreamDestroy(st[k]);
       dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
@@ -90,7 +97,10 @@ struct HostCtx {
       if (dbuf[k]) cudaFree(dbuf[k]);
       if (pin_in[k]) cudaFreeHost(pin_in[k]);
       if (pin_out[k]) cudaFreeHost(pin_out[k]);
+      if (dcode[k]) cudaFree(dcode[k]);
+      if (pcode[k]) cudaFreeHost(pcode[k]);
       dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
+      dcode[k] = pcode[k] = nullptr;
     }
     chunk_cap = 0;
     const size_t bytes = sizeof(float) * (size_t)elems;
@@ -98,6 +108,8 @@ struct HostCtx {
       cudaError_t e = cudaMalloc(&dbuf[k], bytes);
       if (e == cudaSuccess) e = cudaMallocHost(&pin_in[k], bytes);
       if (e == cudaSuccess) e = cudaMallocHost(&pin_out[k], bytes);
+      if (e == cudaSuccess) e = cudaMalloc(&dcode[k], (size_t)elems);
+      if (e == cudaSuccess) e = cudaMallocHost(&pcode[k], (size_t)elems);
       if (e != cudaSuccess) return e;
     }
     chunk_cap = elems;
@@ -158,27 +170,30 @@ class CopyPool {
   }
   int width() const { return (int)workers_.size() + 1; }
 
-  void run(char* dst, const char* src, size_t bytes, int parts) {
-    const size_t part = (bytes / parts + 63) & ~size_t(63);
+  // count units (bytes, or codes when lut) split over `parts` threads; a
+  // unit of the destination is dst_unit bytes
+  void run(char* dst, const char* src, size_t count, int parts, const float* lut = nullptr) {
+    const size_t dst_unit = lut ? sizeof(float) : 1;
+    const size_t part = (count / parts + 63) & ~size_t(63);
     std::unique_lock<std::mutex> lk(mu_);
     jobs_.clear();
     for (int t = 1; t < parts; ++t) {
       const size_t b = part * t;
-      if (b >= bytes) break;
-      jobs_.push_back(Job{dst + b, src + b, std::min(part, bytes - b)});
+      if (b >= count) break;
+      jobs_.push_back(Job{dst + b * dst_unit, src + b, std::min(part, count - b), lut});
     }
     next_ = 0;
     pending_ = jobs_.size();
     ++gen_;
     lk.unlock();
     cv_.notify_all();
-    std::memcpy(dst, src, std::min(part, bytes));
+    exec(Job{dst, src, std::min(part, count), lut});
     lk.lock();
     // help with whatever the workers have not picked up, then wait
     while (next_ < jobs_.size()) {
       const Job j = jobs_[next_++];
       lk.unlock();
-      std::memcpy(j.dst, j.src, j.len);
+      exec(j);
       lk.lock();
       --pending_;
     }
@@ -189,8 +204,18 @@ class CopyPool {
   struct Job {
     char* dst;
     const char* src;
-    size_t len;
+    size_t len;          // bytes (copy) or codes (decode)
+    const float* lut;    // decode: float dst[i] = lut[uint8 src[i]]
   };
+  static void exec(const Job& j) {
+    if (!j.lut) {
+      std::memcpy(j.dst, j.src, j.len);
+      return;
+    }
+    float* d = reinterpret_cast<float*>(j.dst);
+    const uint8_t* c = reinterpret_cast<const uint8_t*>(j.src);
+    for (size_t i = 0; i < j.len; ++i) d[i] = j.lut[c[i]];
+  }
   CopyPool() {
     const unsigned hw = std::thread::hardware_concurrency();
     const int n = (int)std::max(1u, std::min(hw, 16u)) - 1;
@@ -213,7 +238,7 @@ class CopyPool {
       while (next_ < jobs_.size()) {
         const Job j = jobs_[next_++];
         lk.unlock();
-        std::memcpy(j.dst, j.src, j.len);
+        exec(j);
         lk.lock();
         if (--pending_ == 0) done_.notify_all();
       }
@@ -247,6 +272,56 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     return;
   }
   pool.run(static_cast<char*>(dst), static_cast<const char*>(src), bytes, parts);
+}
+
+// dst[i] = lut[codes[i]] over the copy pool (256K codes = 1 MB of output
+// per part, like the copies)
+void parallel_decode(float* dst, const uint8_t* codes, size_t n, const float* lut) {
+  const size_t kMinPart = size_t(1) << 18;
+  const size_t want = std::max<size_t>(1, n / kMinPart);
+  std::lock_guard<std::mutex> lk(g_copy_mu);
+  CopyPool& pool = CopyPool::get();
+  const int parts = (int)std::min<size_t>(want, (size_t)pool.width());
+  pool.run(reinterpret_cast<char*>(dst), reinterpret_cast<const char*>(codes), n, parts, lut);
+}
+
+// One-byte codes for the device->host copy of quantized results: saturating
+// fixed point with wl <= 8 and float formats with 1 + exp + man <= 8, under
+// NearestEven / Stochastic (whose zero results are +0 for fixed point; the
+// float code keeps the sign, so a passed-through -0 survives).  Every
+// quantized value of those formats is one of <= 256 bit patterns; the code
+// is a bijection on them and the host decodes with a 256-entry table, so the
+// output is bit-identical to copying the fp32 values -- at a quarter of the
+// PCIe bytes.
+bool byte_code_for(const lpq_format* f, int mode, ByteCode* bc, float* lut) {
+  if (mode != kNearestEven && mode != kStochastic) return false;
+  if (f->kind == LPQ_FIXED && f->saturate && f->wl <= 8) {
+    bc->kind = 1;
+    bc->scale = std::ldexp(1.0f, f->fl);
+    const float down = std::ldexp(1.0f, -f->fl);
+    for (int c = 0; c < 256; ++c) lut[c] = (float)(int8_t)(uint8_t)c * down + 0.0f;
+    return true;
+  }
+  if (f->kind == LPQ_FLOAT && 1 + f->exp_bits + f->man_bits <= 8 && f->exp_bits >= 2) {
+    const int bias = (1 << (f->exp_bits - 1)) - 1;
+    bc->kind = 2;
+    bc->man = f->man_bits;
+    bc->min_exp = 1 - bias;
+    const int nexp = 1 << f->exp_bits;  // E code 0 = zero, 1.. = min_exp..
+    for (int c = 0; c < 256; ++c) {
+      const int sign = (c >> 7) & 1;
+      const int ei = (c >> f->man_bits) & (nexp - 1);
+      const int mt = c & ((1 << f->man_bits) - 1);
+      float v = 0.0f;
+      if (ei != 0) {
+        const int e = bc->min_exp + ei - 1;
+        v = std::ldexp(1.0f + (float)mt / (float)(1 << f->man_bits), e);
+      }
+      lut[c] = sign ? -v : v;
+    }
+    return true;
+  }
+  return false;
 }
 
 int resolve_device(int device, lpq_status* st) {
@@ -289,13 +364,15 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
   lpq_format fr = *f;
   if (rows) fr.block_dim = 0;
   lpq_status qst = LPQ_OK;
+  ByteCode bc{};
+  float lut[256];
+  const bool coded = !rows && byte_code_for(f, mode, &bc, lut);
   auto finish = [&](int64_t ci) {
     const int k = (int)(ci % kStreams);
     cudaEventSynchronize(c->done[k]);
-    if (!pin_y) {
-      const int64_t off = ci * chunk, len = std::min(chunk, n - off);
-      parallel_memcpy(y + off, c->pin_out[k], sizeof(float) * (size_t)len);
-    }
+    const int64_t off = ci * chunk, len = std::min(chunk, n - off);
+    if (coded) parallel_decode(y + off, c->pcode[k], (size_t)len, lut);
+    else if (!pin_y) parallel_memcpy(y + off, c->pin_out[k], sizeof(float) * (size_t)len);
   };
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     const int k = (int)(ci % kStreams);
@@ -317,7 +394,13 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
                           index_base + (uint64_t)off, &fr, mode, seed, call,
                           nullptr, 0, c->d_status, c->st[k]);
     if (qst != LPQ_OK) break;
-    LPQ_TRY(cudaMemcpyAsync(dst, c->dbuf[k], bytes, cudaMemcpyDeviceToHost, c->st[k]));
+    if (coded) {  // a quarter of the bytes across PCIe; decoded in finish()
+      LPQ_TRY(launch_encode8(c->dbuf[k], c->dcode[k], len, bc, c->st[k]));
+      LPQ_TRY(cudaMemcpyAsync(c->pcode[k], c->dcode[k], (size_t)len,
+                              cudaMemcpyDeviceToHost, c->st[k]));
+    } else {
+      LPQ_TRY(cudaMemcpyAsync(dst, c->dbuf[k], bytes, cudaMemcpyDeviceToHost, c->st[k]));
+    }
     LPQ_TRY(cudaEventRecord(c->done[k], c->st[k]));
   }
   for (int64_t ci = std::max<int64_t>(0, nchunks - kStreams); ci < nchunks; ++ci)
@@ -510,5 +593,14 @@ lpq_status lpq_quantize_composed_host(const float* x, float* y,
 }
 
 void lpq_shutdown(void) { lpq::shutdown_contexts(); }
+
+void lpq_host_bytes_per_element(const lpq_format* f, int mode, int* h2d, int* d2h) {
+  lpq::ByteCode bc{};
+  float lut[256];
+  const bool coded = f && lpq::check_format(f) == LPQ_OK && f->kind != LPQ_BLOCK &&
+                     lpq::byte_code_for(f, mode, &bc, lut);
+  if (h2d) *h2d = 4;
+  if (d2h) *d2h = coded ? 1 : 4;
+}
 
 }  // extern "C"

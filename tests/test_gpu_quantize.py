@@ -556,3 +556,29 @@ def test_index_base_device_path(q, oracle, base):
                                   index_base=base)
         st, want = oracle.quantize(x, ofmt, STOCHASTIC, seed=6, call=2, index_base=base)
         assert st == 0 and same_bits(got, want), (fmt, base)
+
+
+@pytest.mark.parametrize("fmt_name", ["fixed84", "fixed41sym", "fixed8m3", "float52", "float43",
+                                      "float21", "float34"])
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
+def test_host_path_byte_codes(q, fmt_name, mode):
+    # tensors > 16 MB take the chunked host pipeline, which for these formats
+    # copies one-byte codes device->host and decodes them on the host: the
+    # result must equal the device path bit for bit (signed zeros, saturation,
+    # the underflow grid, pageable and page-locked outputs)
+    fmt = {"fixed84": q.FixedFormat(8, 4), "fixed41sym": q.FixedFormat(4, 1, True),
+           "fixed8m3": q.FixedFormat(8, -3), "float52": q.FloatFormat(5, 2),
+           "float43": q.FloatFormat(4, 3), "float21": q.FloatFormat(2, 1),
+           "float34": q.FloatFormat(3, 4)}[fmt_name]
+    rng = np.random.default_rng(len(fmt_name) * 7 + mode)
+    n = 5_000_001
+    x = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-30, 30, n)).astype(np.float32)
+    x[:16] = [0.0, -0.0, 1e-30, -1e-30, 3.4e38, -3.4e38, 1.0, -1.0, 0.5, -0.5,
+              114688.0, -114688.0, 2.0**-14, -2.0**-14, 2.0**-15, -2.0**-15]
+    spec = q.QuantSpec(fmt, q.RoundingMode(mode), 11)
+    want = q.quantize_fused_at(dev(x), spec, 4).cpu().numpy()
+    got = q.quantize_fused_at(x, spec, 4)  # pageable numpy -> host path
+    assert same_bits(got, want), (fmt_name, mode)
+    xp = torch.from_numpy(x).pin_memory()
+    got_p = q.quantize_fused_at(xp, spec, 4)
+    assert same_bits(got_p.numpy(), want), (fmt_name, mode)
