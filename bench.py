@@ -510,6 +510,35 @@ def run_gemm(args, rank, world, local_rank):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_t = sms * 128 * 2 * 1.965e9 / 1e12
     ach = flops * args.steps / el / 1e12
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the per-op GEMM is not in the reference: its restatement (oracle/,
+        # the definition the tests check against), rows split over the host
+        # threads (ctypes releases the GIL), on a sample of output rows
+        try:
+            import time as _t
+            from concurrent.futures import ThreadPoolExecutor
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_lib import Oracle, float_fmt
+            o = Oracle()
+            th = cpu_threads()
+            rows = 2 * th
+            ah = a[:rows].cpu().numpy()
+            bh = b.cpu().numpy()
+            f87o = float_fmt(8, 7)
+            t_0 = _t.perf_counter()
+            with ThreadPoolExecutor(th) as ex:
+                list(ex.map(lambda r: o.quant_gemm(ah[r:r + 2], bh, f87o, f87o),
+                            range(0, rows, 2)))
+            secs = _t.perf_counter() - t_0
+            cpu = {"value": round(2.0 * rows * N * K / secs / 1e9, 4), "unit": "GFLOP/s",
+                   "cores": th, "kind": "port",
+                   "sample": f"{rows} output rows of the 4096^3 problem through the restated "
+                             f"per-op GEMM (oracle/lpq_oracle.c; the reference has none), "
+                             f"{th} threads", "cpu_model": cpu_model()}
+        except Exception as e:  # the baseline must not sink the GPU line
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "port",
+                   "sample": f"unavailable: {e}"}
     return {
         "metric": "quant-GEMM GFLOP/s (per-op rounded, float(8,7) after every multiply and add)",
         "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
@@ -523,7 +552,7 @@ def run_gemm(args, rank, world, local_rank):
                      "peak": round(peak_t, 2), "unit": "TFLOP/s",
                      "frac": round(ach / peak_t, 4), "traffic": None,
                      "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz"},
-        "clocks": clk.summary(),
+        "cpu_baseline": cpu, "clocks": clk.summary(),
     }
 
 
@@ -568,6 +597,29 @@ def run_matmul_q(args, rank, world, local_rank):
         el = float(t.item())
     flops = 2.0 * M * N * K
     ach = flops * args.steps / el / 1e12
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the reference's own quantized_matmul (oracle/_ref) on 32 rows of
+        # the problem (its matmul runs serially below m = 4096)
+        try:
+            import time as _t
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_lib import RefLib, fixed_fmt
+            ref = RefLib()
+            ref.set_num_threads(cpu_threads())
+            rows = 32
+            ah = a[:rows].cpu().numpy()
+            bh = b.cpu().numpy()
+            t_0 = _t.perf_counter()
+            ref.quantized_matmul(ah, bh, fixed_fmt(8, 4), 0, seed=SEED, call=0)
+            secs = _t.perf_counter() - t_0
+            cpu = {"value": round(2.0 * rows * N * K / secs / 1e9, 4), "unit": "GFLOP/s",
+                   "cores": 1, "kind": "reference",
+                   "sample": f"lpsim::quantized_matmul on {rows} rows x 4096 x 4096 "
+                             f"(oracle/_ref; serial below m = 4096)", "cpu_model": cpu_model()}
+        except Exception as e:
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
     return {
         "metric": "reference quantized_matmul GFLOP/s (double accumulation, fused quantize epilogue)",
         "value": round(flops * world * args.steps / el / 1e9, 1), "unit": "GFLOP/s",
@@ -583,7 +635,7 @@ def run_matmul_q(args, rank, world, local_rank):
                      "peak_source": "measured in-repo: register-resident DMMA m8n8k4 loop on "
                                     "this B200 (scripts/dmma_rate.cu; DFMA: 33.4); "
                                     "MEASURED_PEAKS.json has no FP64 figure"},
-        "clocks": clk.summary(),
+        "cpu_baseline": cpu, "clocks": clk.summary(),
     }
 
 
