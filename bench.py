@@ -758,6 +758,28 @@ def run_sweep(args, rank, world, local_rank):
     peak, peak_src, _ = load_peaks()
     ach = nbytes * args.steps / el / 1e9
     total_elems = sum(t.numel() for t, _ in tensors)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the reference's quantize_fused_at on a bounded sample of the sweep:
+        # 20 per-sample rows of the first activation ([20, 802816] = 16M
+        # floats) through the three formats, all host threads
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_lib import block_fmt, fixed_fmt, float_fmt
+            th = cpu_threads()
+            act = tensors[2][0]
+            xh = act.reshape(act.shape[0], -1)[:20].contiguous().cpu().numpy()
+            secs = 0.0
+            for fo in (float_fmt(5, 2), fixed_fmt(8, 4), block_fmt(8, 0)):
+                secs += cpu_reference_time(fo, 1, xh.reshape(-1), xh.shape, th, 1)
+            cpu = {"value": round(3 * 8 * xh.size / secs / 1e9, 4), "unit": "GB/s",
+                   "cores": th, "kind": "reference",
+                   "sample": f"lpsim::quantize_fused_at, nearest, float(5,2) + fixed(8,4) + "
+                             f"block(8, dim0) on {xh.shape} of the first activation, "
+                             f"{th} threads", "cpu_model": cpu_model()}
+        except Exception as e:
+            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
     return {
         "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
         "value": round(ach * world, 2), "unit": "GB/s", "n_gpus": world,
@@ -776,7 +798,7 @@ def run_sweep(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
                      "peak_source": peak_src},
-        "clocks": clk.summary(),
+        "cpu_baseline": cpu, "clocks": clk.summary(),
     }
 
 
