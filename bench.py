@@ -191,6 +191,16 @@ CONFIGS = {
     "c1n": dict(workload="C1: float exp=5 man=2, nearest-even, 2^24 elements per GPU "
                          "(rotating buffers > L2)",
                 kind="float", n=1 << 24, fmt=("float", 5, 2), mode="nearest_even"),
+    "c1log": dict(workload="C1 log-uniform variant (SURVEY 8(d)): float exp=5 man=2, "
+                           "stochastic, 2^24 elements with |x| log-uniform in "
+                           "[2^-20, 2^20] and random sign (underflow and saturation "
+                           "branches; rotating buffers > L2)",
+                  kind="float", n=1 << 24, fmt=("float", 5, 2), mode="stochastic",
+                  dist="loguniform"),
+    "c1logn": dict(workload="C1 log-uniform variant: float exp=5 man=2, nearest-even, "
+                            "2^24 elements, |x| log-uniform in [2^-20, 2^20]",
+                   kind="float", n=1 << 24, fmt=("float", 5, 2), mode="nearest_even",
+                   dist="loguniform"),
     "c1big": dict(workload="float exp=5 man=2, stochastic, 2^30 elements (diagnostic)",
                   kind="float", n=1 << 30, fmt=("float", 5, 2), mode="stochastic"),
     "c2": dict(workload="C2: fixed-point wl=8 fl=4 saturating, stochastic rounding, "
@@ -252,6 +262,12 @@ def run_ours(args, rank, world, local_rank):
         nbuf = max(2, (512 << 20) // (n * 8))
     xs = [q.random_uniform(shape, 2 + i, 0, -10.0, 10.0, device=dev, index_base=base)
           for i in range(nbuf)]
+    if cfg.get("dist") == "loguniform":  # |x| = 2^U(-20, 20), random sign
+        xs = [torch.copysign(torch.exp2(q.random_uniform(shape, 50 + i, 0, -20.0, 20.0,
+                                                         device=dev, index_base=base)),
+                             q.random_uniform(shape, 60 + i, 0, -1.0, 1.0, device=dev,
+                                              index_base=base))
+              for i in range(nbuf)]
     if cfg["kind"] == "block":  # per-row exponents vary
         g = torch.Generator(device=dev).manual_seed(rank)
         sc = torch.exp2(torch.randint(-20, 21, (cfg["rows"], 1), device=dev,

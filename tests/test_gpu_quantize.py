@@ -279,6 +279,22 @@ def test_c1_float52_16M_full(q, oracle):
         assert st == 0 and np.array_equal(bits(got), bits(want))
 
 
+def test_c1_float52_16M_loguniform(q, oracle):
+    """SURVEY 8(d) C1 variant: |x| log-uniform in [2^-20, 2^20], random sign --
+    the underflow two-point grid, the saturation clamp and the bit-domain /
+    scaled-form switch inside float4s all occur."""
+    n = 1 << 24
+    e = q.random_uniform((n,), 50, 0, -20.0, 20.0)
+    s = q.random_uniform((n,), 60, 0, -1.0, 1.0)
+    x = torch.copysign(torch.exp2(e), s)
+    xh = x.cpu().numpy()
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        spec = q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode(mode), 0x15EED)
+        got = q.quantize_fused_at(x, spec, 0).cpu().numpy()
+        st, want = oracle.quantize(xh, float_fmt(5, 2), mode, seed=0x15EED, call=0)
+        assert st == 0 and np.array_equal(bits(got), bits(want))
+
+
 def test_c2_fixed84_1G_windows(q, oracle):
     n = 1 << 30
     x = q.random_uniform((n,), 2, 0, -10.0, 10.0)
