@@ -391,12 +391,17 @@ void launch_general(const float* A, const float* B, float* C, int64_t M,
 // double, so chaining the MMAs over k in ascending order is bit-identical to
 // the reference's `acc += double(a) * double(b)` (tensor.cpp:355-376).
 // Padding k beyond K adds +-0 products, which leave a (never -0) accumulator
-// unchanged.  128x128 CTA tile, 8 warps of 64x32 (8x4 MMA tiles, 64 double
-// accumulators per thread), K staged by 16 as double in double-buffered
-// shared memory with conflict-free padded strides; 0.375 B of shared-memory
-// traffic per MAC instead of the CUDA-core DFMA tile's 2 B (which capped it at
-// 17.4 TFLOP/s, smem-bandwidth-bound).
-constexpr int kDM = 128, kDN = 128, kDK = 16, kDT = 256;
+// unchanged.  128x64 CTA tile, 8 warps of 32x32 (4x4 MMA tiles, 32 double
+// accumulators per thread, <= 128 registers), TWO CTAs per SM so one CTA's
+// barrier bubble is filled by the other's MMAs; K staged by 32 as double in
+// double-buffered shared memory (108.5 KB per CTA) with conflict-free padded
+// fragment strides.  Measured on B200 (ncu): DMMA sub-pipe 82 % active with
+// one 128x128 CTA per SM (8 or 16 warps, K by 16) -> 91 % with this shape;
+// 29.6 -> 33.2 TFLOP/s.  (The CUDA-core DFMA tile, 2 B of shared-memory
+// traffic per MAC, was capped at 17.4.)
+constexpr int kDM = 128, kDN = 64, kDK = 32, kDT = 256;
+constexpr int kWTM = 4, kWTN = 4;  // 8x8 MMA tiles per warp: 32 x 32 outputs
+constexpr int kDWN = kDN / (8 * kWTN);  // warps along n
 constexpr int kDAS = kDK + 4;   // A row stride (doubles): conflict-free fragments
 constexpr int kDBS = kDN + 4;   // B row stride (doubles)
 constexpr size_t kDSmem = sizeof(double) * 2 * ((size_t)kDM * kDAS + (size_t)kDK * kDBS);
@@ -428,7 +433,7 @@ struct EpilogueNone {
 };
 
 template <int M_, class Epi, bool VEC>
-__global__ void __launch_bounds__(kDT)
+__global__ void __launch_bounds__(kDT, 2)
     k_matmul_q(const float* __restrict__ A, const float* __restrict__ B,
                float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                int64_t row_base, Epi epi, uint64_t key,
@@ -437,47 +442,57 @@ __global__ void __launch_bounds__(kDT)
   double* As = dsm;                              // [2][kDM][kDAS]
   double* Bs = dsm + 2 * kDM * kDAS;             // [2][kDK][kDBS]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wm = warp >> 2, wn = warp & 3;       // 2 x 4 warps of 64 x 32
+  const int wm = warp / kDWN, wn = warp % kDWN;  // 4 x 2 warps of 32 x 32
   const int64_t m0 = (int64_t)blockIdx.y * kDM, n0 = (int64_t)blockIdx.x * kDN;
-  double acc[8][4][2];
+  double acc[kWTM][kWTN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kWTM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // global -> register staging: A 128 rows x 16 k (8 floats per thread),
-  // B 16 k-rows x 128 cols (8 floats per thread)
-  float ra[8], rb[8];
-  auto load = [&](int64_t k0) {
-    const int64_t ar = m0 + (t >> 1), ak = k0 + (t & 1) * 8;
-    const int64_t bk = k0 + (t >> 4), bn = n0 + (t & 15) * 8;
-    if (VEC && ar < M && ak + 8 <= K) {  // K % 4 == 0, 16-byte aligned rows
-      const float4 u = __ldg(reinterpret_cast<const float4*>(A + ar * K + ak));
-      const float4 w = __ldg(reinterpret_cast<const float4*>(A + ar * K + ak + 4));
-      ra[0] = u.x; ra[1] = u.y; ra[2] = u.z; ra[3] = u.w;
-      ra[4] = w.x; ra[5] = w.y; ra[6] = w.z; ra[7] = w.w;
+    for (int j = 0; j < kWTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // global -> register staging in float4 chunks: A 128 rows x kDK k,
+  // B kDK k-rows x 64 cols
+  constexpr int kAQ = kDM * kDK / 4 / kDT, kBQ = kDK * kDN / 4 / kDT;
+  constexpr int kAC = kDK / 4, kBC = kDN / 4;     // chunks per smem row
+  float4 ra[kAQ], rb[kBQ];
+  auto ld4 = [&](const float* p, int64_t r, int64_t c, int64_t R, int64_t Cn) {
+    float4 v;
+    if (VEC && r < R && c + 4 <= Cn) {  // Cn % 4 == 0, 16-byte aligned rows
+      v = __ldg(reinterpret_cast<const float4*>(p + r * Cn + c));
     } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        ra[q] = (ar < M && ak + q < K) ? __ldg(A + ar * K + ak + q) : 0.0f;
+      v.x = (r < R && c < Cn) ? __ldg(p + r * Cn + c) : 0.0f;
+      v.y = (r < R && c + 1 < Cn) ? __ldg(p + r * Cn + c + 1) : 0.0f;
+      v.z = (r < R && c + 2 < Cn) ? __ldg(p + r * Cn + c + 2) : 0.0f;
+      v.w = (r < R && c + 3 < Cn) ? __ldg(p + r * Cn + c + 3) : 0.0f;
     }
-    if (VEC && bk < K && bn + 8 <= N) {  // N % 4 == 0
-      const float4 u = __ldg(reinterpret_cast<const float4*>(B + bk * N + bn));
-      const float4 w = __ldg(reinterpret_cast<const float4*>(B + bk * N + bn + 4));
-      rb[0] = u.x; rb[1] = u.y; rb[2] = u.z; rb[3] = u.w;
-      rb[4] = w.x; rb[5] = w.y; rb[6] = w.z; rb[7] = w.w;
-    } else {
+    return v;
+  };
+  auto load = [&](int64_t k0) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        rb[q] = (bk < K && bn + q < N) ? __ldg(B + bk * N + bn + q) : 0.0f;
+    for (int q = 0; q < kAQ; ++q) {
+      const int c = t + kDT * q;
+      ra[q] = ld4(A, m0 + c / kAC, k0 + (c % kAC) * 4, M, K);
+    }
+#pragma unroll
+    for (int q = 0; q < kBQ; ++q) {
+      const int c = t + kDT * q;
+      rb[q] = ld4(B, k0 + c / kBC, n0 + (c % kBC) * 4, K, N);
     }
   };
   auto stash = [&](int buf) {
-    double* a = As + buf * kDM * kDAS + (t >> 1) * kDAS + (t & 1) * 8;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = (double)ra[q];
-    double* b = Bs + buf * kDK * kDBS + (t >> 4) * kDBS + (t & 15) * 8;
+    for (int q = 0; q < kAQ; ++q) {
+      const int c = t + kDT * q;
+      double2* a = reinterpret_cast<double2*>(As + buf * kDM * kDAS + (c / kAC) * kDAS + (c % kAC) * 4);
+      a[0] = make_double2((double)ra[q].x, (double)ra[q].y);
+      a[1] = make_double2((double)ra[q].z, (double)ra[q].w);
+    }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) b[q] = (double)rb[q];
+    for (int q = 0; q < kBQ; ++q) {
+      const int c = t + kDT * q;
+      double2* b = reinterpret_cast<double2*>(Bs + buf * kDK * kDBS + (c / kBC) * kDBS + (c % kBC) * 4);
+      b[0] = make_double2((double)rb[q].x, (double)rb[q].y);
+      b[1] = make_double2((double)rb[q].z, (double)rb[q].w);
+    }
   };
   const int64_t nk = (K + kDK - 1) / kDK;
   load(0);
@@ -487,19 +502,19 @@ __global__ void __launch_bounds__(kDT)
   for (int64_t kt = 0; kt < nk; ++kt) {
     const int buf = (int)(kt & 1);
     if (kt + 1 < nk) load((kt + 1) * kDK);
-    const double* a_s = As + buf * kDM * kDAS + (wm * 64 + fr) * kDAS + fk;
-    const double* b_s = Bs + buf * kDK * kDBS + fk * kDBS + wn * 32 + fr;
+    const double* a_s = As + buf * kDM * kDAS + (wm * 8 * kWTM + fr) * kDAS + fk;
+    const double* b_s = Bs + buf * kDK * kDBS + fk * kDBS + wn * 8 * kWTN + fr;
 #pragma unroll
     for (int ks = 0; ks < kDK / 4; ++ks) {       // ascending k, 4 per MMA
-      double af[8], bf[4];
+      double af[kWTM], bf[kWTN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = a_s[i * 8 * kDAS + ks * 4];
+      for (int i = 0; i < kWTM; ++i) af[i] = a_s[i * 8 * kDAS + ks * 4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = b_s[ks * 4 * kDBS + j * 8];
+      for (int j = 0; j < kWTN; ++j) bf[j] = b_s[ks * 4 * kDBS + j * 8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < kWTM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kWTN; ++j)
           asm volatile(
               "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
               : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]) : "d"(af[i]), "d"(bf[j]));
@@ -510,14 +525,14 @@ __global__ void __launch_bounds__(kDT)
   // epilogue: lane holds D[fr][2*fk + {0,1}] of every 8x8 tile
   uint32_t bad = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + wm * 64 + i * 8 + fr;
+  for (int i = 0; i < kWTM; ++i) {
+    const int64_t row = m0 + wm * 8 * kWTM + i * 8 + fr;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kWTN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t col = n0 + wn * 32 + j * 8 + 2 * fk + h;
+        const int64_t col = n0 + wn * 8 * kWTN + j * 8 + 2 * fk + h;
         if (col >= N) continue;
         const float c = __double2float_rn(acc[i][j][h]);
         uint32_t v = 0;
