@@ -118,6 +118,27 @@ lpq_status lpq_quantize(const float* x, float* y, const int64_t* shape,
                         int mode, uint64_t seed, uint64_t call, void* ws,
                         size_t ws_bytes, uint32_t* d_status, void* stream);
 
+/* Block formats split across shards (a whole-tensor block, or
+ * blocks along dim d >= 1 of a tensor sharded along dim 0) need ONE exchange
+ * step: every shard reduces its part of each block's maximum, the maxima are
+ * combined with an elementwise max across shards (ncclAllReduce(MAX) on
+ * `extent` uint32s: non-negative float bits order like the floats), then
+ * every shard quantizes with the global maxima.  Both halves of fused_block
+ * (proj/src/quant_ops.cpp:68-115; reduce_max_abs, tensor.cpp:320-353).
+ *   lpq_block_absmax: maxima[extent] := max|x| bits over this tensor's part
+ *     of each block (NaN ignored; extent = shape[block_dim], 1 for the whole
+ *     tensor).  Device uint32 array, overwritten.
+ *   lpq_quantize_block_apply: the quantization pass with the given maxima;
+ *     index_base as in lpq_quantize (the shard's first global flat index).
+ *     Flags non-finite inputs and out-of-range maxima in *d_status. */
+lpq_status lpq_block_absmax(const float* x, const int64_t* shape, int rank,
+                            const lpq_format* f, uint32_t* maxima, void* stream);
+lpq_status lpq_quantize_block_apply(const float* x, float* y, const int64_t* shape,
+                                    int rank, uint64_t index_base,
+                                    const lpq_format* f, int mode, uint64_t seed,
+                                    uint64_t call, const uint32_t* maxima,
+                                    uint32_t* d_status, void* stream);
+
 /* Synchronise `stream`, read and clear *d_status, map the bits to a status
  * (LPQ_ERR_BLOCK_RANGE takes precedence over LPQ_ERR_INVALID_INPUT, as the
  * reference's reduction pass throws before its quantization pass). */

@@ -210,6 +210,57 @@ int lpqo_reduce_max_abs(const float* x, const int64_t* shape, int rank,
   return LPQO_OK;
 }
 
+int lpqo_quantize_block_given_max(const float* x, float* y, const int64_t* shape,
+                                  int rank, uint64_t index_base,
+                                  const lpqo_format* f, int mode, uint64_t seed,
+                                  uint64_t call, const float* mx) {
+  /* fused_block pass 2 (quant_ops.cpp:73-115) with the block maxima given */
+  int st = lpqo_validate(f);
+  if (st) return st;
+  if (f->kind != LPQO_BLOCK) return LPQO_UNSUPPORTED;
+  if (f->block_dim >= 0 && f->block_dim >= rank) return LPQO_SHAPE_ERROR;
+  int64_t n = o_numel(shape, rank);
+  uint64_t key = lpqo_stream_key(seed, call);
+  int bad = 0;
+  int64_t blocks = f->block_dim < 0 ? 1 : shape[f->block_dim];
+  double* delta = (double*)malloc(sizeof(double) * (size_t)(blocks ? blocks : 1));
+  double* inv = (double*)malloc(sizeof(double) * (size_t)(blocks ? blocks : 1));
+  for (int64_t b = 0; b < blocks; ++b) {
+    if (mx[b] == 0.0f) { delta[b] = 0.0; inv[b] = 0.0; continue; }
+    int E = o_float_exponent(mx[b]);
+    if (E > 126) { /* check_block_range, scalar_quant.hpp:72-77 */
+      free(delta); free(inv);
+      return LPQO_INVALID_INPUT;
+    }
+    int shift = E - (f->wl - 2);
+    delta[b] = p2(shift);
+    inv[b] = p2(-shift);
+  }
+  int64_t stride = 1, extent = 1;
+  if (f->block_dim >= 0) {
+    extent = shape[f->block_dim];
+    for (int d = f->block_dim + 1; d < rank; ++d) stride *= shape[d];
+  }
+  double kmax = (double)((1ll << (f->wl - 1)) - 1);
+  double kmin = -p2(f->wl - 1);
+  for (int64_t i = 0; i < n; ++i) {
+    float v = x[i];
+    if (!isfinite(v)) { bad = 1; y[i] = 0.0f; continue; }
+    int64_t b = f->block_dim < 0 ? 0 : (i / stride) % extent;
+    if (delta[b] == 0.0) { y[i] = 0.0f; continue; }
+    double u = mode == LPQO_STOCHASTIC
+                   ? (double)lpqo_variate_from_key(key, index_base + (uint64_t)i)
+                   : 0.0;
+    /* block_quant_one_m, scalar_quant.hpp:80-87 */
+    double k = lpqo_round_integer((double)v * inv[b], mode, u);
+    if (k > kmax) k = kmax;
+    if (k < kmin) k = kmin;
+    y[i] = (float)(k * delta[b]);
+  }
+  free(delta); free(inv);
+  return bad ? LPQO_INVALID_INPUT : LPQO_OK;
+}
+
 int lpqo_quantize(const float* x, float* y, const int64_t* shape, int rank,
                   uint64_t index_base, const lpqo_format* f, int mode,
                   uint64_t seed, uint64_t call) {
@@ -219,47 +270,15 @@ int lpqo_quantize(const float* x, float* y, const int64_t* shape, int rank,
   uint64_t key = lpqo_stream_key(seed, call);
   int bad = 0;
   if (f->kind == LPQO_BLOCK) {
-    /* fused_block, quant_ops.cpp:68-115 */
+    /* fused_block, quant_ops.cpp:68-115: pass 1 (the maxima), pass 2 */
     if (f->block_dim >= 0 && f->block_dim >= rank) return LPQO_SHAPE_ERROR;
     int64_t blocks = f->block_dim < 0 ? 1 : shape[f->block_dim];
     float* mx = (float*)malloc(sizeof(float) * (size_t)(blocks ? blocks : 1));
-    double* delta = (double*)malloc(sizeof(double) * (size_t)(blocks ? blocks : 1));
-    double* inv = (double*)malloc(sizeof(double) * (size_t)(blocks ? blocks : 1));
     lpqo_reduce_max_abs(x, shape, rank, f->block_dim, mx);
-    for (int64_t b = 0; b < blocks; ++b) {
-      if (mx[b] == 0.0f) { delta[b] = 0.0; inv[b] = 0.0; continue; }
-      int E = o_float_exponent(mx[b]);
-      if (E > 126) { /* check_block_range, scalar_quant.hpp:72-77 */
-        free(mx); free(delta); free(inv);
-        return LPQO_INVALID_INPUT;
-      }
-      int shift = E - (f->wl - 2);
-      delta[b] = p2(shift);
-      inv[b] = p2(-shift);
-    }
-    int64_t stride = 1, extent = 1;
-    if (f->block_dim >= 0) {
-      extent = shape[f->block_dim];
-      for (int d = f->block_dim + 1; d < rank; ++d) stride *= shape[d];
-    }
-    double kmax = (double)((1ll << (f->wl - 1)) - 1);
-    double kmin = -p2(f->wl - 1);
-    for (int64_t i = 0; i < n; ++i) {
-      float v = x[i];
-      if (!isfinite(v)) { bad = 1; y[i] = 0.0f; continue; }
-      int64_t b = f->block_dim < 0 ? 0 : (i / stride) % extent;
-      if (delta[b] == 0.0) { y[i] = 0.0f; continue; }
-      double u = mode == LPQO_STOCHASTIC
-                     ? (double)lpqo_variate_from_key(key, index_base + (uint64_t)i)
-                     : 0.0;
-      /* block_quant_one_m, scalar_quant.hpp:80-87 */
-      double k = lpqo_round_integer((double)v * inv[b], mode, u);
-      if (k > kmax) k = kmax;
-      if (k < kmin) k = kmin;
-      y[i] = (float)(k * delta[b]);
-    }
-    free(mx); free(delta); free(inv);
-    return bad ? LPQO_INVALID_INPUT : LPQO_OK;
+    st = lpqo_quantize_block_given_max(x, y, shape, rank, index_base, f, mode, seed,
+                                       call, mx);
+    free(mx);
+    return st;
   }
   for (int64_t i = 0; i < n; ++i) {
     float v = x[i];

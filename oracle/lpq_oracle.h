@@ -75,6 +75,13 @@ int lpqo_quantize(const float* x, float* y, const int64_t* shape, int rank,
                   uint64_t index_base, const lpqo_format* f, int mode,
                   uint64_t seed, uint64_t call);
 
+/* fused_block's quantization pass (quant_ops.cpp:73-115) with the block
+   maxima mx[extent] given (e.g. combined across shards). */
+int lpqo_quantize_block_given_max(const float* x, float* y, const int64_t* shape,
+                                  int rank, uint64_t index_base,
+                                  const lpqo_format* f, int mode, uint64_t seed,
+                                  uint64_t call, const float* mx);
+
 /* Per-block maxima as reduce_max_abs (tensor.cpp:320-353): whole tensor
    (block_dim < 0) gives one value. */
 int lpqo_reduce_max_abs(const float* x, const int64_t* shape, int rank,

@@ -103,6 +103,10 @@ _PROTOS = {
                                C.c_int, C.c_uint64, C.c_uint64, _VP,
                                C.c_size_t, _VP, _VP]),
     "lpq_status_fetch": (C.c_int, [_VP, _VP]),
+    "lpq_block_absmax": (C.c_int, [_VP, _I64P, C.c_int, _F, _VP, _VP]),
+    "lpq_quantize_block_apply": (C.c_int, [_VP, _VP, _I64P, C.c_int, C.c_uint64, _F,
+                                           C.c_int, C.c_uint64, C.c_uint64, _VP, _VP,
+                                           _VP]),
     "lpq_quant_gemm_workspace_size": (C.c_size_t, [C.c_int64, C.c_int64,
                                                    C.c_int64]),
     "lpq_quant_gemm": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64,

@@ -477,6 +477,12 @@ int64_t col_rows_per_chunk(int64_t outer, int64_t W) {
 }
 
 template <int M>
+cudaError_t launch_two_pass_m(const float* x, float* y, const BlockGeom& g,
+                              bool segments, bool reduce, uint32_t* maxima,
+                              uint64_t base, uint64_t key, int wl,
+                              uint32_t* status, cudaStream_t s);
+
+template <int M>
 cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
                            BlockPlan plan, uint64_t base, uint64_t key, int wl,
                            void* ws, uint32_t* status, cudaStream_t s) {
@@ -492,23 +498,37 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
   uint32_t* maxima = static_cast<uint32_t*>(ws);
   cudaError_t e = cudaMemsetAsync(maxima, 0, sizeof(uint32_t) * g.extent, s);
   if (e != cudaSuccess) return e;
+  return launch_two_pass_m<M>(x, y, g, plan == BlockPlan::kTwoPassSegments, true,
+                              maxima, base, key, wl, status, s);
+}
+
+// The two-pass plans; reduce == false: maxima[extent] is given (already
+// reduced, e.g. across shards: lpq_quantize_block_apply) and only the
+// quantize pass runs.
+template <int M>
+cudaError_t launch_two_pass_m(const float* x, float* y, const BlockGeom& g,
+                              bool segments, bool reduce, uint32_t* maxima,
+                              uint64_t base, uint64_t key, int wl,
+                              uint32_t* status, cudaStream_t s) {
   const int sms = device_info().sm_count;
-  if (plan == BlockPlan::kTwoPassSegments) {
+  if (segments) {
     const int64_t nseg = g.outer * g.extent;
     const int64_t pieces = (g.stride + kPiece - 1) / kPiece;
     const bool vec = (g.stride % 4 == 0) && aligned16(x) && aligned16(y);
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)sms * 8, nseg * pieces));
     if (vec) {
-      k_seg_reduce<true><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+      if (reduce)
+        k_seg_reduce<true><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
       k_seg_apply<M, true><<<grid, kSegT, 0, s>>>(x, y, nseg, g.stride, g.extent, pieces,
                                                   maxima, base, key, wl, status);
     } else {
-      k_seg_reduce<false><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
+      if (reduce)
+        k_seg_reduce<false><<<grid, kSegT, 0, s>>>(x, nseg, g.stride, g.extent, pieces, maxima);
       k_seg_apply<M, false><<<grid, kSegT, 0, s>>>(x, y, nseg, g.stride, g.extent, pieces,
                                                    maxima, base, key, wl, status);
     }
-    note_launch(2);
+    note_launch(reduce ? 2 : 1);
     return cudaGetLastError();
   }
   const int64_t W = g.extent * g.stride;
@@ -517,15 +537,17 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
   dim3 grid((unsigned)((W + kColTile - 1) / kColTile),
             (unsigned)((g.outer + rpc - 1) / rpc));
   if (vec) {
-    k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+    if (reduce)
+      k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
     k_col_apply<M, true><<<grid, kColT, 0, s>>>(x, y, g.outer, W, g.stride, rpc, maxima,
                                                 base, key, wl, status);
   } else {
-    k_col_reduce<false><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
+    if (reduce)
+      k_col_reduce<false><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
     k_col_apply<M, false><<<grid, kColT, 0, s>>>(x, y, g.outer, W, g.stride, rpc, maxima,
                                                  base, key, wl, status);
   }
-  note_launch(2);
+  note_launch(reduce ? 2 : 1);
   return cudaGetLastError();
 }
 
@@ -559,6 +581,20 @@ cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
   }
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_block_apply(const float* x, float* y, const BlockGeom& g,
+                               const uint32_t* maxima, uint64_t base, uint64_t key,
+                               int wl, int mode, uint32_t* status, cudaStream_t s) {
+  if (g.outer * g.extent * g.stride <= 0) return cudaSuccess;
+  uint32_t* mx = const_cast<uint32_t*>(maxima);  // read only when reduce == false
+  const bool seg = g.stride >= 1024;
+  switch (mode) {
+    case kStochastic: return launch_two_pass_m<kStochastic>(x, y, g, seg, false, mx, base, key, wl, status, s);
+    case kNearestAway: return launch_two_pass_m<kNearestAway>(x, y, g, seg, false, mx, base, key, wl, status, s);
+    case kNearestZero: return launch_two_pass_m<kNearestZero>(x, y, g, seg, false, mx, base, key, wl, status, s);
+    default: return launch_two_pass_m<kNearestEven>(x, y, g, seg, false, mx, base, key, wl, status, s);
+  }
 }
 
 bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y) {

@@ -216,6 +216,51 @@ lpq_status lpq_quantize(const float* x, float* y, const int64_t* shape,
                          ws, ws_bytes, d_status, static_cast<cudaStream_t>(stream));
 }
 
+static lpq_status block_split_args(const float* x, const int64_t* shape, int rank,
+                                   const lpq_format* f, BlockGeom* g, int64_t* n) {
+  lpq_status st = check_format(f);
+  if (st != LPQ_OK) return st;
+  if (f->kind != LPQ_BLOCK) return LPQ_ERR_UNSUPPORTED;
+  st = check_shape(shape, rank, n);
+  if (st != LPQ_OK) return st;
+  st = block_geometry(f, shape, rank, g);
+  if (st != LPQ_OK) return st;
+  if (*n > 0 && (!x || (reinterpret_cast<uintptr_t>(x) & 3u))) return LPQ_ERR_ARGUMENT;
+  return LPQ_OK;
+}
+
+lpq_status lpq_block_absmax(const float* x, const int64_t* shape, int rank,
+                            const lpq_format* f, uint32_t* maxima, void* stream) {
+  BlockGeom g;
+  int64_t n = 0;
+  lpq_status st = block_split_args(x, shape, rank, f, &g, &n);
+  if (st != LPQ_OK) return st;
+  if (g.extent == 0) return LPQ_OK;
+  if (!maxima) return LPQ_ERR_ARGUMENT;
+  // launch_block_reduce zeroes maxima first (an empty part contributes 0)
+  cudaError_t e = launch_block_reduce(x, g, maxima, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
+}
+
+lpq_status lpq_quantize_block_apply(const float* x, float* y, const int64_t* shape,
+                                    int rank, uint64_t index_base,
+                                    const lpq_format* f, int mode, uint64_t seed,
+                                    uint64_t call, const uint32_t* maxima,
+                                    uint32_t* d_status, void* stream) {
+  BlockGeom g;
+  int64_t n = 0;
+  lpq_status st = block_split_args(x, shape, rank, f, &g, &n);
+  if (st != LPQ_OK) return st;
+  if (mode < 0 || mode > 3) return LPQ_ERR_ARGUMENT;
+  if (n == 0) return LPQ_OK;
+  if (!y || !maxima || !d_status || (reinterpret_cast<uintptr_t>(y) & 3u))
+    return LPQ_ERR_ARGUMENT;
+  cudaError_t e = launch_block_apply(x, y, g, maxima, index_base, stream_key(seed, call),
+                                     f->wl, mode, d_status, static_cast<cudaStream_t>(stream));
+  note_passes(1);
+  return e == cudaSuccess ? LPQ_OK : cuda_fail(e);
+}
+
 lpq_status lpq_status_fetch(uint32_t* d_status, void* stream) {
   if (!d_status) return LPQ_ERR_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

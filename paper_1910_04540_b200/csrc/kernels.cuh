@@ -65,6 +65,10 @@ cudaError_t launch_block(const float* x, float* y, const BlockGeom& g,
 
 cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
                                 uint32_t* maxima, cudaStream_t s);
+// the quantize pass alone, with maxima[extent] given (max|x| bits per block)
+cudaError_t launch_block_apply(const float* x, float* y, const BlockGeom& g,
+                               const uint32_t* maxima, uint64_t base, uint64_t key,
+                               int wl, int mode, uint32_t* status, cudaStream_t s);
 
 // ---- generators -------------------------------------------------------------
 // One-byte codes of quantized values for the host path's device->host copy

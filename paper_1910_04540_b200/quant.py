@@ -243,6 +243,65 @@ def quantize_fused_at(t, spec: QuantSpec, call: int, *, out=None,
     return _quantize_host(t, spec, call, index_base=index_base)
 
 
+def _block_extent(x, fmt):
+    if not isinstance(fmt, BlockFloatFormat):
+        raise UnsupportedFormatError("block maxima need a block format")
+    if fmt.block_dim is None:
+        return 1
+    if fmt.block_dim >= x.dim():
+        raise ShapeError("block_dim out of range")
+    return int(x.shape[fmt.block_dim])
+
+
+def block_absmax(t, fmt: "BlockFloatFormat"):
+    """This tensor's part of every block maximum of `fmt` (the first half of
+    fused_block, quant_ops.cpp:68-115; reduce_max_abs, tensor.cpp:320-353):
+    an int32 CUDA tensor [extent] of max|x| fp32 bits (NaN ignored).  For a
+    block split across shards, combine the shards' results with an
+    elementwise max (torch.distributed.all_reduce(op=MAX)), then call
+    quantize_block_apply -- lpq_block_absmax in include/lpq.h."""
+    x = t.contiguous()
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise TypeError("block_absmax: a float32 CUDA tensor is required")
+    extent = _block_extent(x, fmt)
+    m = torch.zeros(max(extent, 1), dtype=torch.int32, device=x.device)
+    f = fmt.c()
+    with torch.cuda.device(x.device):
+        check(lib.lpq_block_absmax(C.c_void_p(x.data_ptr()), shape_array(x.shape), x.dim(),
+                                   C.byref(f), C.c_void_p(m.data_ptr()),
+                                   _stream_ptr(x.device)), "block_absmax")
+    return m[:extent]
+
+
+def quantize_block_apply(t, spec: QuantSpec, call: int, maxima, *, out=None,
+                         index_base: int = 0, sync: bool = True):
+    """The quantization pass of fused_block with given block maxima (e.g.
+    all-reduced across shards); bit-identical to quantize_fused_at of the
+    whole tensor when `maxima` are the whole tensor's block maxima and
+    `index_base` is this shard's first global flat index."""
+    x = t.contiguous()
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise TypeError("quantize_block_apply: a float32 CUDA tensor is required")
+    extent = _block_extent(x, spec.format)
+    m = maxima.to(device=x.device, dtype=torch.int32).contiguous()
+    if m.numel() != extent:
+        raise ValueError(f"maxima: {extent} block maxima expected, got {m.numel()}")
+    if out is not None:
+        _check_out(out, x)
+    y = torch.empty_like(x) if out is None else out
+    f = spec.format.c()
+    with torch.cuda.device(x.device):
+        st = lib.lpq_quantize_block_apply(
+            C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), shape_array(x.shape),
+            x.dim(), int(index_base), C.byref(f), int(spec.mode), int(spec.seed), int(call),
+            C.c_void_p(m.data_ptr()), C.c_void_p(_status_buf(x.device).data_ptr()),
+            _stream_ptr(x.device))
+        check(st, "quantize")
+        if sync:
+            fetch_status(x.device)
+    return y
+
+
 def quantize_fused(t, spec: QuantSpec, **kw):
     """quantize_fused (quant_ops.cpp:179-183): uses and (for stochastic
     rounding only) advances spec.call_counter."""
@@ -469,7 +528,7 @@ __all__ = [
     "RoundingMode", "FloatFormat", "FixedFormat", "BlockFloatFormat",
     "NumberFormat", "QuantSpec", "validate", "quantize_fused",
     "quantize_fused_at", "quantize_fused_many", "quantize_composed",
-    "quantize_composed_at",
+    "quantize_composed_at", "block_absmax", "quantize_block_apply",
     "quantized_op", "quantized_matmul",
     "quantized_matmul_at", "quant_gemm", "random_uniform", "variate_tensor",
     "pass_count", "reset_pass_count", "launch_count", "fetch_status",

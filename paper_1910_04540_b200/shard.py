@@ -30,7 +30,8 @@ def shard_range(n: int, rank: int, world: int, unit: int = 1):
 def block_unit(shape, block_dim):
     """Elements per shardable unit for a block format: a whole block row
     (block_dim == 0 on any shape); None when blocks span the tensor (whole
-    tensor / inner dims), which needs a max-exchange step instead."""
+    tensor / inner dims), which needs the max-exchange step of
+    quantize_block_split instead."""
     if block_dim is None:
         return None
     if block_dim == 0:
@@ -44,6 +45,27 @@ def block_unit(shape, block_dim):
 def quantize_shard(q, x_local, spec, call, index_base):
     """Quantize this rank's shard (device tensor) of a larger tensor."""
     return q.quantize_fused_at(x_local, spec, call, index_base=index_base)
+
+
+def quantize_block_split(q, x_local, spec, call, index_base, group=None):
+    """A block format whose blocks span shards: the whole
+    tensor (block_dim None; any flat sharding) or blocks along dim d >= 1 of a
+    tensor sharded along dim 0 (whole dim-0 slices per rank).  One exchange
+    step: each rank reduces its part of every block maximum on the device
+    (lpq_block_absmax), the [extent] maxima are combined with ONE
+    all_reduce(MAX) over NCCL (non-negative fp32 bits order like the floats),
+    and each rank quantizes its shard with the global maxima
+    (lpq_quantize_block_apply) -- bit-identical to quantizing the gathered
+    tensor on one GPU (fused_block, quant_ops.cpp:68-115)."""
+    import torch.distributed as dist
+    fmt = spec.format
+    if fmt.block_dim == 0:
+        raise ValueError("block_dim 0: blocks are whole dim-0 slices; shard by rows "
+                         "(block_unit) and quantize locally, no exchange needed")
+    m = q.block_absmax(x_local, fmt)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    return q.quantize_block_apply(x_local, spec, call, m, index_base=index_base)
 
 
 def gather(y_local, group=None):

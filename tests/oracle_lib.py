@@ -86,6 +86,9 @@ class Oracle:
                                     C.POINTER(Fmt), C.c_int, C.c_uint64,
                                     C.c_uint64]
         L.lpqo_reduce_max_abs.argtypes = [_fp, _i64p, C.c_int, C.c_int, _fp]
+        L.lpqo_quantize_block_given_max.argtypes = [_fp, _fp, _i64p, C.c_int, C.c_uint64,
+                                                    C.POINTER(Fmt), C.c_int, C.c_uint64,
+                                                    C.c_uint64, _fp]
         L.lpqo_random_uniform.argtypes = [_fp, C.c_int64, C.c_uint64,
                                           C.c_uint64, C.c_uint64, C.c_float,
                                           C.c_float]
@@ -115,6 +118,15 @@ class Oracle:
         st = self.L.lpqo_quantize(x.reshape(-1) if x.ndim == 0 else x, y,
                                   shape, x.ndim, index_base, C.byref(fmt),
                                   mode, seed, call)
+        return st, y
+
+    def quantize_block_given_max(self, x, fmt, mode, mx, seed=0, call=0, index_base=0):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        y = np.empty_like(x)
+        mx = np.ascontiguousarray(mx, dtype=np.float32)
+        st = self.L.lpqo_quantize_block_given_max(
+            x, y, np.array(x.shape, dtype=np.int64), x.ndim, index_base, C.byref(fmt),
+            mode, seed, call, mx)
         return st, y
 
     def reduce_max_abs(self, x, dim):

@@ -295,6 +295,53 @@ def test_c1_float52_16M_loguniform(q, oracle):
         assert st == 0 and np.array_equal(bits(got), bits(want))
 
 
+@pytest.mark.parametrize("shape,dim,shards", [
+    ((8, 300, 5), None, 2), ((4, 7, 2048), None, 4), ((8, 300, 5), 1, 2),
+    ((4, 7, 2048), 1, 4), ((6, 3, 4, 9), 2, 3), ((6, 3, 4, 9), 3, 2)], ids=str)
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
+def test_block_split_across_shards(q, shape, dim, shards, mode):
+    """blocks spanning shards (whole tensor, or block_dim >= 1 of
+    a tensor sharded along dim 0).  Per-shard lpq_block_absmax, the maxima
+    combined by elementwise max (what all_reduce(MAX) does across ranks),
+    then lpq_quantize_block_apply per shard with its index_base: bitwise the
+    single-tensor quantize_fused_at."""
+    from paper_1910_04540_b200.shard import quantize_block_split
+    x = q.random_uniform(shape, 21, 0, -2.0, 2.0)
+    x[0].view(-1)[3] = 40.0  # the global maximum lives in shard 0 only
+    spec = q.QuantSpec(q.BlockFloatFormat(8, dim), q.RoundingMode(mode), 99)
+    whole = q.quantize_fused_at(x, spec, 5)
+    parts = list(torch.chunk(x, shards, dim=0))
+    m = torch.stack([q.block_absmax(p, spec.format) for p in parts]).amax(0)
+    ref_m = (x.abs().amax(dim=tuple(d for d in range(x.dim()) if d != dim))
+             if dim is not None else x.abs().amax().reshape(1))
+    assert torch.equal(m.view(torch.float32), ref_m.float().reshape(-1))
+    got, base = [], 0
+    for p in parts:
+        got.append(q.quantize_block_apply(p, spec, 5, m, index_base=base))
+        base += p.numel()
+    assert torch.equal(torch.cat(got).view(torch.int32), whole.view(torch.int32))
+    if dim != 0:  # one rank (no process group): the split path is the whole tensor
+        one = quantize_block_split(q, x, spec, 5, 0)
+        assert torch.equal(one.view(torch.int32), whole.view(torch.int32))
+
+
+def test_block_split_errors(q):
+    x = torch.ones(4, 8, device="cuda")
+    spec = q.QuantSpec(q.BlockFloatFormat(8, 1), q.RoundingMode.NearestEven, 1)
+    with pytest.raises(q.UnsupportedFormatError):
+        q.block_absmax(x, q.FixedFormat(8, 4))
+    with pytest.raises(ValueError):
+        q.quantize_block_apply(x, spec, 0, torch.zeros(3, dtype=torch.int32, device="cuda"))
+    x[1, 2] = float("nan")
+    m = q.block_absmax(x, spec.format)
+    assert torch.equal(m.view(torch.float32), torch.ones(8, device="cuda"))  # NaN ignored
+    with pytest.raises(q.InvalidInputError):
+        q.quantize_block_apply(x, spec, 0, m)
+    big = torch.full((8,), 0x7F000000, dtype=torch.int32, device="cuda")  # 2^127
+    with pytest.raises(q.InvalidInputError):
+        q.quantize_block_apply(torch.ones(4, 8, device="cuda"), spec, 0, big)
+
+
 def test_c2_fixed84_1G_windows(q, oracle):
     n = 1 << 30
     x = q.random_uniform((n,), 2, 0, -10.0, 10.0)

@@ -54,8 +54,32 @@ def _worker(rank, world, port, out):
         st, wb = o.quantize(wx, block_fmt(8, 0), STOCHASTIC, seed=9, call=2)
         gb = np.concatenate([p[1] for p in sorted(parts_b, key=lambda t: t[0])])
         ok.append(bool(np.array_equal(bits(gb), bits(wb))))
-        # max-over-ranks timing reduction, as bench.py does
-        t = torch.tensor([1.0 + rank])
+    # blocks spanning shards: the exchange step of
+    # shard.quantize_block_split -- local maxima, ONE all_reduce(MAX), apply
+    # with the global maxima and the shard's index_base -- here with the
+    # oracle's two halves of fused_block in place of the device kernels
+    G = (6, 5, 7)  # global shape, sharded along dim 0
+    per = (G[0] // world) * G[1] * G[2]
+    xs = o.random_uniform(per, 4, 0, -3.0, 3.0, index_base=rank * per)
+    xs = xs.reshape(G[0] // world, G[1], G[2])
+    xs[0, 2, 3] = 50.0 if rank == 1 else xs[0, 2, 3]  # a block max on rank 1 only
+    split = []
+    for dim in (None, 1, 2):
+        st, mx = o.reduce_max_abs(xs, dim)
+        mt = torch.from_numpy(mx.copy())
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        st, ys = o.quantize_block_given_max(xs, block_fmt(8, dim), STOCHASTIC, mt.numpy(),
+                                            seed=11, call=4, index_base=rank * per)
+        gl = [None] * world
+        dist.all_gather_object(gl, (rank, ys, xs))
+        split.append(gl)
+    if rank == 0:
+        for dim, gl in zip((None, 1, 2), split):
+            gl = sorted(gl, key=lambda t: t[0])
+            wx = np.concatenate([g[2] for g in gl])
+            st, want = o.quantize(wx, block_fmt(8, dim), STOCHASTIC, seed=11, call=4)
+            got = np.concatenate([g[1] for g in gl])
+            ok.append(bool(st == 0 and np.array_equal(bits(got), bits(want))))
         out.put(ok)
     t = torch.tensor([1.0 + rank], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -76,7 +100,7 @@ def test_sharded_equals_whole_world2():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert ok == [True, True]
+    assert ok == [True, True, True, True, True]
     assert tmax == 2.0
 
 
