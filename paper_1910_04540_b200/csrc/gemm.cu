@@ -29,10 +29,10 @@
 //    because the product of two fp32 values is exact in double.
 #include <cuda_runtime.h>
 
-#include <cstdint>
-
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdint>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -552,13 +552,18 @@ template <int M_, class Epi>
 void launch_mmq(const float* A, const float* B, float* C, int64_t M, int64_t N,
                 int64_t K, int64_t row_base, const Epi& epi, uint64_t key,
                 uint32_t* status, cudaStream_t s) {
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  // the dynamic shared-memory opt-in is per device: one bit per device that
+  // has it (per instantiation; setting it twice from racing threads is benign)
+  static std::atomic<uint64_t> ready{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(ready.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(k_matmul_q<M_, Epi, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmem);
     cudaFuncSetAttribute(k_matmul_q<M_, Epi, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDSmem);
-    attr = true;
+    ready.fetch_or(bit, std::memory_order_release);
   }
   dim3 grid((unsigned)((N + kDN - 1) / kDN), (unsigned)((M + kDM - 1) / kDM));
   const bool vec = K % 4 == 0 && N % 4 == 0 && aligned16(A) && aligned16(B);
