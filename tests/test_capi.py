@@ -98,3 +98,31 @@ def test_shape_checks_before_any_device_work():
     bf = q.BlockFloatFormat(8, 2).c()
     assert L.lpq_quantize(None, None, _lib.shape_array((4, 4)), 2, 0, C.byref(bf), 0, 0, 0,
                           None, 0, None, None) == _lib.ERR_SHAPE  # block_dim >= rank
+
+
+def test_block_split_entry_points_validate_first():
+    # lpq_block_absmax / lpq_quantize_block_apply: format, shape and argument
+    # errors before any device work
+    from paper_1910_04540_b200 import _lib
+    import paper_1910_04540_b200 as q
+    L = _lib.lib
+    shp = _lib.shape_array((4, 6))
+    fx = q.FixedFormat(8, 4).c()
+    b1 = q.BlockFloatFormat(8, 1).c()
+    b5 = q.BlockFloatFormat(8, 5).c()
+    bad = q.BlockFloatFormat(30, 1).c()
+    assert L.lpq_block_absmax(None, shp, 2, C.byref(fx), None, None) == _lib.ERR_UNSUPPORTED
+    assert L.lpq_block_absmax(None, shp, 2, C.byref(b5), None, None) == _lib.ERR_SHAPE
+    assert L.lpq_block_absmax(None, shp, 2, C.byref(bad), None, None) == _lib.ERR_FORMAT
+    assert L.lpq_block_absmax(None, shp, 2, C.byref(b1), None, None) == _lib.ERR_ARGUMENT
+    assert L.lpq_block_absmax(None, _lib.shape_array((0, 6)), 2, C.byref(b1), None,
+                              None) == _lib.ERR_ARGUMENT  # extent 6 still needs maxima
+
+    def apply(fmt, shape, mode=0):
+        return L.lpq_quantize_block_apply(None, None, _lib.shape_array(shape), len(shape), 0,
+                                          C.byref(fmt), mode, 0, 0, None, None, None)
+    assert apply(fx, (4, 6)) == _lib.ERR_UNSUPPORTED
+    assert apply(b5, (4, 6)) == _lib.ERR_SHAPE
+    assert apply(b1, (4, 6), mode=7) == _lib.ERR_ARGUMENT
+    assert apply(b1, (0, 6)) == 0  # empty: nothing to do
+    assert apply(b1, (4, 6)) == _lib.ERR_ARGUMENT
