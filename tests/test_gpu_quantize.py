@@ -325,6 +325,24 @@ def test_block_split_across_shards(q, shape, dim, shards, mode):
         assert torch.equal(one.view(torch.int32), whole.view(torch.int32))
 
 
+def test_block_split_whole_tensor_2p26(q):
+    """The exchange path at scale: a 2^26-element whole-tensor block split
+    into 4 flat shards equals the single-tensor quantization (both modes)."""
+    n = 1 << 26
+    x = q.random_uniform((n,), 33, 0, -8.0, 8.0)
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        spec = q.QuantSpec(q.BlockFloatFormat(8), q.RoundingMode(mode), 0x15EED)
+        whole = q.quantize_fused_at(x, spec, 1)
+        parts = list(torch.chunk(x, 4))
+        m = torch.stack([q.block_absmax(p, spec.format) for p in parts]).amax(0)
+        out = torch.empty_like(x)
+        base = 0
+        for p, o in zip(parts, torch.chunk(out, 4)):
+            q.quantize_block_apply(p, spec, 1, m, out=o, index_base=base)
+            base += p.numel()
+        assert torch.equal(out.view(torch.int32), whole.view(torch.int32))
+
+
 def test_block_split_errors(q):
     x = torch.ones(4, 8, device="cuda")
     spec = q.QuantSpec(q.BlockFloatFormat(8, 1), q.RoundingMode.NearestEven, 1)
