@@ -207,11 +207,50 @@ __device__ __forceinline__ void quant4(float (&x)[kSgdV], const Slot& s, uint64_
       for (int q = 0; q < kSgdV; ++q) v[q] = variate24(key, idx + q);
     }
   }
+  constexpr int MF = MS == kOff ? kNearestEven : MS;
 #pragma unroll
-  for (int q = 0; q < kSgdV; ++q) {
+  for (int q = 0; q < kSgdV; ++q)
     if (nonfinite(x[q])) flags |= kStatusNonFinite;
-    x[q] = q_mode<MS == kOff ? kNearestEven : MS>(x[q], s, v[q]);
+  // the slot's format dispatch once per 4 elements (uniform), not per
+  // element; float slots take the bit-domain form when none of the 4 is in
+  // the underflow range (as FloatOp::apply4 in elementwise.cu), same results
+  // as q_mode per element
+  if (s.kind == LPQ_FLOAT) {
+    const FloatParams& p = s.fp;
+    if (p.bits_ok && (p.scaled_ok || !p.tiny)) {
+      float c[kSgdV];
+      bool under = false;
+#pragma unroll
+      for (int q = 0; q < kSgdV; ++q) {
+        c[q] = fminf(fmaxf(x[q], -p.max_value), p.max_value);
+        under |= fabsf(c[q]) < p.min_normal && c[q] != 0.0f;
+      }
+      if (!under) {
+#pragma unroll
+        for (int q = 0; q < kSgdV; ++q) x[q] = quant_float_bits<MF>(c[q], p, v[q]);
+        return;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kSgdV; ++q) {
+      if (p.scaled_ok) x[q] = quant_float_scaled<MF>(x[q], p, v[q]);
+      else if (!p.tiny) x[q] = quant_float_fast<MF>(x[q], p, v[q]);
+      else x[q] = quant_float<MF>(x[q], p, v[q]);
+    }
+    return;
   }
+  if (s.saturate) {
+    if (s.xp.tiny) {
+#pragma unroll
+      for (int q = 0; q < kSgdV; ++q) x[q] = quant_fixed<MF, true, true>(x[q], s.xp, v[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSgdV; ++q) x[q] = quant_fixed_sat_fast<MF>(x[q], s.xp, v[q]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kSgdV; ++q) x[q] = quant_fixed<MF, false>(x[q], s.xp, v[q]);
 }
 
 template <int MG, int MA, int MW>
