@@ -81,11 +81,14 @@ class LowPrecisionOptimizer:
     def accumulators(self):
         return self.acc
 
-    def step(self, grads: Sequence) -> None:
+    def step(self, grads: Sequence, *, sync: bool = True) -> None:
         """LowPrecisionOptimizer::step (train.cpp:148-178): every parameter's
         update in one grouped launch (lpq_sgd_step_grouped, up to 64 tensors
         per launch), with the call ids the reference's per-parameter loop
-        would give each of its four quantizations."""
+        would give each of its four quantizations.  sync=True (the
+        reference's behaviour) raises a non-finite update before returning;
+        sync=False leaves the launch asynchronous and the error in the device
+        status word for the next synchronising call (fetch_status)."""
         if len(grads) != len(self.params):
             raise ShapeError("optimizer step: gradient count mismatch")
         if not self.params:
@@ -130,4 +133,5 @@ class LowPrecisionOptimizer:
                                       C.c_void_p(_status_buf(dev).data_ptr()),
                                       _stream_ptr(dev))
         check(st, "optimizer step")
-        fetch_status(dev)
+        if sync:
+            fetch_status(dev)

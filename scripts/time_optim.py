@@ -34,4 +34,12 @@ torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) / reps * 1e3
 ms = e0.elapsed_time(e1) / reps
 print(f"{len(params)} tensors, {n} params: {ms:.3f} ms/step (device), {wall:.3f} ms (wall), "
-      f"{24 * n / ms / 1e6:.0f} GB/s algorithmic")
+      f"{24 * n / ms / 1e6:.0f} GB/s algorithmic (step(sync=True): status read every step)")
+e0.record()
+for _ in range(reps):
+    opt.step(grads, sync=False)
+e1.record()
+torch.cuda.synchronize()
+q.fetch_status()
+ms = e0.elapsed_time(e1) / reps
+print(f"step(sync=False), back to back: {ms:.3f} ms/step, {24 * n / ms / 1e6:.0f} GB/s algorithmic")

@@ -119,3 +119,33 @@ def test_sgd_step_rejects_block_and_bad_args():
         opt.step([torch.ones(8, device="cuda")])
     with pytest.raises(q.ShapeError):
         LowPrecisionOptimizer(p, 0.1, 0.5).step([torch.ones(9, device="cuda")])
+
+
+def test_sgd_step_async_equals_sync_and_defers_errors():
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200.optim import LowPrecisionOptimizer
+    S, E = q.RoundingMode.Stochastic, q.RoundingMode.NearestEven
+    specs = dict(weight=q.QuantSpec(q.FixedFormat(8, 6), E),
+                 accumulator=q.QuantSpec(q.FloatFormat(8, 7), S, 2),
+                 gradient=q.QuantSpec(q.FixedFormat(8, 12), S, 3))
+    import copy
+    shapes = [(300,), (17, 33), (4096,)]
+    rng = np.random.default_rng(3)
+    init = [rng.uniform(-0.5, 0.5, s).astype(np.float32) for s in shapes]
+    pa = [torch.from_numpy(p.copy()).cuda() for p in init]
+    pb = [torch.from_numpy(p.copy()).cuda() for p in init]
+    oa = LowPrecisionOptimizer(pa, lr=0.05, momentum=0.9, **copy.deepcopy(specs))
+    ob = LowPrecisionOptimizer(pb, lr=0.05, momentum=0.9, **copy.deepcopy(specs))
+    for _ in range(3):
+        grads = [torch.from_numpy(rng.normal(0, 0.01, s).astype(np.float32)).cuda()
+                 for s in shapes]
+        oa.step(grads)
+        ob.step(grads, sync=False)
+    q.fetch_status()
+    for a, b in zip(pa, pb):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    bad = [torch.full(s, float("inf"), device="cuda") for s in shapes]
+    ob.step(bad, sync=False)  # no exception yet: the launch is asynchronous
+    with pytest.raises(q.InvalidInputError):
+        q.fetch_status()
+    q.fetch_status()  # the status word was cleared
