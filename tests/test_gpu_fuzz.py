@@ -1,0 +1,85 @@
+"""Randomised GPU parity sweep: random formats (every field over its valid
+range), rounding modes, shapes (rank 1-4, ragged), block dimensions, index
+bases, call ids, input distributions (log-uniform magnitudes over the whole
+fp32 range, exact rounding ties, zeros and signed zeros) and buffer
+misalignment, each quantized through the C ABI and compared bit for bit with
+the C restatement of the reference (tests/oracle_lib.py).  Seeded: a failing
+case prints its seed and reproduces."""
+import numpy as np
+import pytest
+
+from oracle_lib import block_fmt, bits, fixed_fmt, float_fmt
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    kind = int(rng.integers(0, 3))
+    if kind == 0:
+        e = int(rng.integers(1, 9))
+        m = int(rng.integers(0, 24))
+        fmt = float_fmt(e, m)
+        scale = 2.0 ** int(rng.integers(-20, 21))
+    elif kind == 1:
+        wl = int(rng.integers(2, 25))
+        fl = int(rng.integers(-12, 30)) if rng.random() < 0.85 else \
+            int(rng.choice([wl - 128, 126, -100, 100]))
+        fmt = fixed_fmt(wl, fl, bool(rng.random() < 0.3), bool(rng.random() < 0.7))
+        scale = 2.0 ** float(wl - 1 - fl + rng.integers(-3, 3))
+    else:
+        fmt = None  # block: needs the shape first
+        scale = 2.0 ** int(rng.integers(-60, 60))
+    rank = int(rng.integers(1, 5))
+    shape = tuple(int(rng.integers(1, {1: 5000, 2: 300, 3: 40, 4: 16}[rank]))
+                  for _ in range(rank))
+    if kind == 2:
+        dim = int(rng.integers(-1, rank))
+        fmt = block_fmt(int(rng.integers(2, 25)), None if dim < 0 else dim)
+    n = int(np.prod(shape))
+    with np.errstate(over="ignore"):  # huge fixed-point ranges: inf, filtered below
+        x = (rng.uniform(-1, 1, n) * scale).astype(np.float32)
+    r = rng.random(n)
+    wide = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-149, 127, n)).astype(np.float32)
+    x = np.where(r < 0.15, wide, x)
+    if kind == 1:  # exact ties of the fixed-point grid
+        ties = ((rng.integers(-2 ** (fmt.wl - 1), 2 ** (fmt.wl - 1), n) + 0.5)
+                * 2.0 ** -fmt.fl).astype(np.float32)
+        x = np.where((r > 0.85) & (r < 0.95) & np.isfinite(ties), ties, x)
+    x = np.where(r > 0.98, np.float32(0.0), x)
+    x = np.where(r > 0.99, np.float32(-0.0), x).astype(np.float32)
+    x = x[np.isfinite(x)] if kind != 2 else np.nan_to_num(x, posinf=1.0, neginf=-1.0)
+    x = np.resize(x, n).astype(np.float32).reshape(shape)
+    mode = int(rng.integers(0, 4))
+    base = int(rng.choice([0, int(rng.integers(1, 2 ** 20)), 2 ** 40 + int(rng.integers(0, 4))]))
+    call = int(rng.integers(0, 2 ** 31))
+    offset = int(rng.integers(0, 4)) if rank == 1 else 0
+    return fmt, mode, x, base, call, offset
+
+
+@pytest.mark.parametrize("chunk", range(8))
+def test_random_formats_shapes_modes(chunk):
+    import paper_1910_04540_b200 as q
+    from oracle_lib import Oracle
+    o = Oracle()
+    for seed in range(chunk * 60, (chunk + 1) * 60):
+        fmt, mode, x, base, call, offset = _random_case(seed)
+        if fmt.kind == 0:
+            f = q.FloatFormat(fmt.exp_bits, fmt.man_bits)
+        elif fmt.kind == 1:
+            f = q.FixedFormat(fmt.wl, fmt.fl, bool(fmt.symmetric), bool(fmt.saturate))
+        else:
+            f = q.BlockFloatFormat(fmt.wl, None if fmt.block_dim < 0 else fmt.block_dim)
+        spec = q.QuantSpec(f, q.RoundingMode(mode), 0xC0FFEE + seed, 0)
+        st, want = o.quantize(x, fmt, mode, seed=0xC0FFEE + seed, call=call, index_base=base)
+        buf = torch.empty(x.size + 4, device="cuda")
+        xd = buf[offset:offset + x.size].view(x.shape)
+        xd.copy_(torch.from_numpy(x))
+        if st != 0:  # the reference raises (e.g. block maximum out of range)
+            with pytest.raises(q.InvalidInputError):
+                q.quantize_fused_at(xd, spec, call, index_base=base)
+            continue
+        got = q.quantize_fused_at(xd, spec, call, index_base=base).cpu().numpy()
+        assert np.array_equal(bits(got), bits(want)), (seed, repr(fmt), mode, x.shape, base)
