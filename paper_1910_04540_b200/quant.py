@@ -283,7 +283,10 @@ def quantize_block_apply(t, spec: QuantSpec, call: int, maxima, *, out=None,
     if x.dtype != torch.float32 or not x.is_cuda:
         raise TypeError("quantize_block_apply: a float32 CUDA tensor is required")
     extent = _block_extent(x, spec.format)
-    m = maxima.to(device=x.device, dtype=torch.int32).contiguous()
+    if not isinstance(maxima, torch.Tensor) or maxima.dtype != torch.int32:
+        raise TypeError("maxima: the int32 fp32-bit tensor block_absmax returns "
+                        "(combine shards with an elementwise max of those bits)")
+    m = maxima.to(device=x.device).contiguous()
     if m.numel() != extent:
         raise ValueError(f"maxima: {extent} block maxima expected, got {m.numel()}")
     if out is not None:

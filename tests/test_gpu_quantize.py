@@ -350,6 +350,8 @@ def test_block_split_errors(q):
         q.block_absmax(x, q.FixedFormat(8, 4))
     with pytest.raises(ValueError):
         q.quantize_block_apply(x, spec, 0, torch.zeros(3, dtype=torch.int32, device="cuda"))
+    with pytest.raises(TypeError):  # float maxima would be converted, not reinterpreted
+        q.quantize_block_apply(x, spec, 0, torch.ones(8, device="cuda"))
     x[1, 2] = float("nan")
     m = q.block_absmax(x, spec.format)
     assert torch.equal(m.view(torch.float32), torch.ones(8, device="cuda"))  # NaN ignored
