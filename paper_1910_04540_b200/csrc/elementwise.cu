@@ -220,7 +220,7 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   // stochastic 1764 -> 2032)
   const bool small = idx4 && n < (int64_t(1) << 26);
   constexpr int kUnrollSmall = unroll_small<M>();
-  if (M == kStochastic && small) {
+  if constexpr (M == kStochastic) if (small) {  // (not instantiated for other modes)
     // stochastic (issue-heavier) small tensors: 5, 6 or 7 float4 per thread,
     // whichever fills the last wave of 4 CTAs/SM best (2^24 float(5,2): 7,
     // 3.96 waves, 4864 -> 4947 GB/s vs 6 at 4.61 waves)
