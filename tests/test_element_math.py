@@ -142,3 +142,58 @@ def test_block_math_vs_oracle(hm, oracle, wl, mode):
             continue
         assert st == 0 and not badblk
         assert np.array_equal(bits(got), bits(want)), (wl, mode, e)
+
+
+UNDER_FMTS = [float_fmt(5, 2), float_fmt(2, 1), float_fmt(4, 3), float_fmt(3, 2),
+              float_fmt(7, 12), float_fmt(6, 0), float_fmt(2, 22), float_fmt(8, 7)]
+
+
+def _underflow_cases(fmt):
+    """Inputs at the underflow boundaries of `fmt` and, per input, variates at
+    the stochastic decision boundary (T = |x| * 2^(24 - min_exp))."""
+    min_exp = 1 - ((1 << (fmt.exp_bits - 1)) - 1)
+    half, mn = 2.0 ** (min_exp - 1), 2.0 ** min_exp
+    mags = [half, np.nextafter(np.float32(half), np.float32(0)),
+            np.nextafter(np.float32(half), np.float32(1)),
+            np.nextafter(np.float32(mn), np.float32(0)), mn, 1e-45, 2e-45,
+            2.0 ** (min_exp - 24), 3 * 2.0 ** (min_exp - 24), 2.0 ** (min_exp - 2),
+            (2 ** 24 - 1) * 2.0 ** (min_exp - 24), 1.5 * 2.0 ** (min_exp - 24),
+            0.75 * mn, 0.3 * mn]
+    xs, vs = [], []
+    for m in mags:
+        m = np.float32(m)
+        if not np.isfinite(m) or m == 0:
+            continue
+        t = float(m) * 2.0 ** (24 - min_exp)
+        cand = {0, 1, 2 ** 24 - 1}
+        for c in (np.floor(t), np.ceil(t)):
+            if c < 2 ** 25:
+                c = int(c)
+                cand |= {c - 1, c, c + 1, 2 ** 24 - c - 1, 2 ** 24 - c, 2 ** 24 - c + 1}
+        for v in sorted(c for c in cand if 0 <= c < 2 ** 24):
+            for sgn in (1.0, -1.0):
+                xs.append(np.float32(sgn * m))
+                vs.append(v)
+    return np.array(xs, np.float32), np.array(vs, np.uint32)
+
+
+@pytest.mark.parametrize("fmt", UNDER_FMTS, ids=repr)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_underflow_decision_boundaries(hm, oracle, fmt, mode):
+    """The kernels' element math on the underflow two-point grid against the
+    restated scalar quantizer with the SAME explicit variate u = v * 2^-24, at
+    the round-to-nearest tie and at the stochastic decision boundary on both
+    signs (v = T, T +- 1, 2^24 - T ...); the reference's own scalar API too
+    when oracle/_ref is built."""
+    x, v = _underflow_cases(fmt)
+    got = np.empty_like(x)
+    hm.hm_quant(x, v, got, x.size, C.byref(fmt), mode)
+    u = (v.astype(np.float64) * 2.0 ** -24).astype(np.float32)
+    want = np.array([oracle.quant_scalar(float(a), fmt, mode, float(b)) for a, b in zip(x, u)],
+                    np.float32)
+    bad = bits(got) != bits(want)
+    assert not bad.any(), (x[bad][:4], v[bad][:4], got[bad][:4], want[bad][:4])
+    from oracle_lib import RefLib
+    if RefLib.available():
+        st, ref = RefLib().quant_scalar_many(x, fmt, mode, u if mode == 0 else None)
+        assert st == 0 and np.array_equal(bits(got), bits(ref))
