@@ -114,3 +114,14 @@ def test_shard_range_partitions(n, world, unit):
     assert all((hi - lo) % unit == 0 for lo, hi in spans)
     sizes = [hi - lo for lo, hi in spans]
     assert max(sizes) - min(sizes) <= unit
+
+
+def test_block_split_refuses_row_blocks():
+    # block_dim 0 blocks are whole dim-0 slices: shard by rows, no exchange
+    import paper_1910_04540_b200 as q
+    from paper_1910_04540_b200.shard import block_unit, quantize_block_split
+    spec = q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode.NearestEven, 1)
+    with pytest.raises(ValueError):
+        quantize_block_split(q, None, spec, 0, 0)
+    assert block_unit((4, 5, 6), 0) == 30
+    assert block_unit((4, 5, 6), None) is None and block_unit((4, 5, 6), 2) is None
