@@ -241,6 +241,53 @@ def mode_id(cfg):
     return {"stochastic": 0, "nearest_even": 1}[cfg["mode"]]
 
 
+def make_input(q, cfg, shape, i, dev, base):
+    """Synthetic input of SURVEY §8(d), generated on the device with the
+    reference's own random_uniform (tensor.cpp:430-440, bit-identical), buffer
+    i of the rotating set (i = 0 is the workload's tensor itself):
+      C1 : random_uniform(RngStream{7}, call i, -4, 4)  (bench.cpp:58-60)
+      C2 : random_uniform(RngStream{2}, call i, -10, 10)
+      C3 : random_uniform(RngStream{3}, call i, -1, 1) x 2^s_r per row, s_r an
+           integer uniform in [-20, 20] (random_uniform(RngStream{4}) of the row)
+      log-uniform C1 variant: |x| = 2^U(-20, 20), random sign."""
+    import torch
+    if cfg.get("dist") == "loguniform":  # |x| = 2^U(-20, 20), random sign
+        return torch.copysign(
+            torch.exp2(q.random_uniform(shape, 50, i, -20.0, 20.0, device=dev, index_base=base)),
+            q.random_uniform(shape, 60, i, -1.0, 1.0, device=dev, index_base=base))
+    if cfg["kind"] == "float":
+        return q.random_uniform(shape, 7, i, -4.0, 4.0, device=dev, index_base=base)
+    if cfg["kind"] == "block":
+        rows = shape[0]
+        x = q.random_uniform(shape, 3, i, -1.0, 1.0, device=dev, index_base=base)
+        r0 = base // shape[1]
+        s = torch.floor(q.random_uniform((rows, 1), 4, i, -20.0, 21.0, device=dev,
+                                         index_base=r0)).clamp_(-20, 20)
+        return x * torch.exp2(s)
+    return q.random_uniform(shape, 2, i, -10.0, 10.0, device=dev, index_base=base)
+
+
+def host_input(cfg, shape):
+    """make_input(buffer 0) through the reference library on the host (the
+    --impl reference arm; same values bit for bit)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import RefLib
+    ref = RefLib()
+    if cfg.get("dist") == "loguniform":
+        u = ref.random_uniform(shape, 50, 0, -20.0, 20.0)
+        sg = ref.random_uniform(shape, 60, 0, -1.0, 1.0)
+        return np.copysign(np.exp2(u), sg).astype(np.float32)
+    if cfg["kind"] == "float":
+        return ref.random_uniform(shape, 7, 0, -4.0, 4.0)
+    if cfg["kind"] == "block":
+        x = ref.random_uniform(shape, 3, 0, -1.0, 1.0)
+        s = np.clip(np.floor(ref.random_uniform((shape[0], 1), 4, 0, -20.0, 21.0)), -20, 20)
+        x *= np.exp2(s).astype(np.float32)
+        return x
+    return ref.random_uniform(shape, 2, 0, -10.0, 10.0)
+
+
 # ---------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -260,19 +307,7 @@ def run_ours(args, rank, world, local_rank):
     nbuf = 1
     if n * 4 * 2 < 512 << 20:  # small config: rotate buffers so L2 cannot hold them
         nbuf = max(2, (512 << 20) // (n * 8))
-    xs = [q.random_uniform(shape, 2 + i, 0, -10.0, 10.0, device=dev, index_base=base)
-          for i in range(nbuf)]
-    if cfg.get("dist") == "loguniform":  # |x| = 2^U(-20, 20), random sign
-        xs = [torch.copysign(torch.exp2(q.random_uniform(shape, 50 + i, 0, -20.0, 20.0,
-                                                         device=dev, index_base=base)),
-                             q.random_uniform(shape, 60 + i, 0, -1.0, 1.0, device=dev,
-                                              index_base=base))
-              for i in range(nbuf)]
-    if cfg["kind"] == "block":  # per-row exponents vary
-        g = torch.Generator(device=dev).manual_seed(rank)
-        sc = torch.exp2(torch.randint(-20, 21, (cfg["rows"], 1), device=dev,
-                                      generator=g).float())
-        xs = [x * sc for x in xs]
+    xs = [make_input(q, cfg, shape, i, dev, base) for i in range(nbuf)]
     ys = [torch.empty_like(x) for x in xs]
     stream = torch.cuda.current_stream(dev)
     status = q.quant._status_buf(dev)
@@ -493,15 +528,25 @@ def run_gemm(args, rank, world, local_rank):
     import paper_1910_04540_b200 as q
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    from paper_1910_04540_b200.shard import broadcast_operand, gemm_rows
     M = N = K = 4096
+    # the BASELINE problem (4096^3) split by output rows over the ranks
+    # (strong scaling): rank r owns rows [lo, hi) of A and C, passes
+    # row_base = lo (global variate index), and B is generated once on rank 0
+    # and broadcast, outside the timed region
+    lo, hi = gemm_rows(M, rank, world)
     f87 = q.QuantSpec(q.FloatFormat(8, 7))
-    a = q.quantize_fused_at(q.random_uniform((M, K), 41, 0, -1.0, 1.0, device=dev,
-                                             index_base=rank * M * K), f87, 0)
-    b = q.quantize_fused_at(q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev), f87, 0)
-    c = torch.empty((M, N), device=dev)
+    a = q.quantize_fused_at(q.random_uniform((hi - lo, K), 41, 0, -1.0, 1.0, device=dev,
+                                             index_base=lo * K), f87, 0)
+    if rank == 0:
+        b = q.quantize_fused_at(q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev), f87, 0)
+    else:
+        b = torch.empty((K, N), device=dev)
+    broadcast_operand(b)
+    c = torch.empty((hi - lo, N), device=dev)
     fm = q.FloatFormat(8, 7)
     for _ in range(args.warmup):
-        q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=rank * M)
+        q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=lo)
     q.fetch_status(dev)
     if world > 1:
         dist.barrier()
@@ -512,7 +557,7 @@ def run_gemm(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         t0.record(s)
         for _ in range(args.steps):
-            q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=rank * M)
+            q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=lo)
         t1.record(s)
         torch.cuda.synchronize()
     q.fetch_status(dev)
@@ -521,11 +566,11 @@ def run_gemm(args, rank, world, local_rank):
         t = torch.tensor([el], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
-    flops = 2.0 * M * N * K
-    value = flops * world * args.steps / el / 1e9
+    flops = 2.0 * M * N * K  # the whole problem, all ranks
+    value = flops * args.steps / el / 1e9
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_t = sms * 128 * 2 * 1.965e9 / 1e12
-    ach = flops * args.steps / el / 1e12
+    ach = flops * args.steps / el / 1e12 / world  # per GPU
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the per-op GEMM is not in the reference: its restatement (oracle/,
@@ -560,9 +605,11 @@ def run_gemm(args, rank, world, local_rank):
         "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 ops + bf16 rounding",
-        "data": "synthetic", "config": {"workload": "C4: 4096x4096x4096 per GPU",
-                                        "parallelism": f"shard{world}"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32 ops + bf16 rounding",
+        "data": "synthetic", "config": {"workload": "C4: 4096x4096x4096, output rows split "
+                                                    "over the GPUs, B broadcast from rank 0",
+                                        "rows_per_gpu": hi - lo,
+                                        "parallelism": f"rows{world}"},
         "gpu_launches": q.launch_count() - l0,
         "roofline": {"bound": "fp32_cuda_core", "achieved": round(ach, 2),
                      "peak": round(peak_t, 2), "unit": "TFLOP/s",
@@ -662,87 +709,36 @@ def run_sweep(args, rank, world, local_rank):
     float(5,2), fixed(8,4) and block(8, dim 0) (per output channel for
     weights and gradients, per sample for activations); nearest-even for
     weights and activations, stochastic for gradients.  One step = the whole
-    sweep (486 quantizations), captured once as a CUDA graph and replayed."""
+    sweep (486 quantizations), captured once as a CUDA graph and replayed.
+    At N GPUs the sweep's work units are bin-packed over the ranks by bytes
+    (shard.binpack; strong scaling: the job is one sweep)."""
     import torch
     import torch.distributed as dist
     import ctypes as C
     import paper_1910_04540_b200 as q
-    from paper_1910_04540_b200 import _lib
-    from paper_1910_04540_b200.resnet50 import numel, resnet50_layers
+    from paper_1910_04540_b200.resnet50 import ResNet50Sweep
+    from paper_1910_04540_b200.shard import binpack
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    layers = resnet50_layers(256)
-    fmts = [q.FloatFormat(5, 2), q.FixedFormat(8, 4), q.BlockFloatFormat(8, 0)]
-    tensors = []  # (tensor, mode)
-    for i, (name, wshape, ashape) in enumerate(layers):
-        tensors.append((q.random_uniform(wshape, 100 + i, 0, -0.1, 0.1, device=dev),
-                        q.RoundingMode.NearestEven))
-        tensors.append((q.random_uniform(wshape, 200 + i, 0, -1e-3, 1e-3, device=dev),
-                        q.RoundingMode.Stochastic))
-        tensors.append((q.random_uniform(ashape, 300 + i, 0, -4.0, 4.0, device=dev),
-                        q.RoundingMode.NearestEven))
-    outs = [torch.empty_like(t) for t, _ in tensors]  # weights/grads outputs
-    out_big = torch.empty(max(t.numel() for t, _ in tensors), device=dev)
-    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
-    status = q.quant._status_buf(dev)
-    # weights and gradients: one grouped launch per (kind, format) --
-    # lpq_quantize_grouped, 54 tensors each; activations: one launch each
-    groups, singles, keep = [], [], []
-    for kind in (0, 1):  # 0 weights (nearest), 1 gradients (stochastic)
-        idx = list(range(kind, len(tensors), 3))
-        for f in fmts:
-            descs = (_lib.LpqTensorDesc * len(idx))()
-            for j, i in enumerate(idx):
-                t = tensors[i][0]
-                shp = _lib.shape_array(t.shape)
-                keep.append(shp)
-                descs[j] = _lib.LpqTensorDesc(t.data_ptr(), outs[i].data_ptr(), shp,
-                                              t.dim(), 0, 0, j)
-            groups.append((descs, len(idx), f.c(), int(tensors[kind][1]),
-                           sum(tensors[i][0].numel() for i in idx)))
-    for t, mode in tensors[2::3]:
-        shp = _lib.shape_array(t.shape)
-        for f in fmts:
-            singles.append((C.c_void_p(t.data_ptr()), C.c_void_p(out_big.data_ptr()), shp,
-                            t.dim(), f.c(), int(mode), t.numel()))
-
-    def run_group(g, sp):
-        descs, cnt, fc, mode, n = g
-        _lib.check(_lib.lib.lpq_quantize_grouped(descs, cnt, C.byref(fc), mode, SEED,
-                                                 C.c_void_p(ws.data_ptr()), ws.numel(),
-                                                 C.c_void_p(status.data_ptr()), sp), "sweep")
-
-    def run_single(c, sp):
-        xp, yp, shp, rank_, fc, mode, n = c
-        _lib.check(_lib.lib.lpq_quantize(xp, yp, shp, rank_, 0, C.byref(fc), mode, SEED, 0,
-                                         C.c_void_p(ws.data_ptr()), ws.numel(),
-                                         C.c_void_p(status.data_ptr()), sp), "sweep")
+    mine = binpack(ResNet50Sweep.unit_bytes(256), world)[rank]
+    plan = ResNet50Sweep(q, dev, units=mine)
+    layers = plan.layers
+    tensors = list(plan.inputs.values())
+    s0 = torch.cuda.current_stream(dev)
+    q.reset_pass_count()
+    nbytes = plan.measure_once(C.c_void_p(s0.cuda_stream))
+    launches_per_sweep = plan.launches
+    calls = [None] * (3 * len(tensors))
+    nbytes_all = torch.tensor([float(nbytes)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(nbytes_all)
+    nbytes_all = int(nbytes_all.item())
+    q.fetch_status(dev)
 
     def sweep(stream):
-        sp = C.c_void_p(stream.cuda_stream)
-        for g in groups:
-            run_group(g, sp)
-        for c in singles:
-            run_single(c, sp)
+        plan.launch(C.c_void_p(stream.cuda_stream))
 
-    # algorithmic bytes from the passes the library makes (8 B/elem single
-    # pass, 12 B/elem two-pass block plans)
-    q.reset_pass_count()
-    l0 = q.launch_count()
-    nbytes = 0
-    s0 = torch.cuda.current_stream(dev)
-    sp0 = C.c_void_p(s0.cuda_stream)
-    for g in groups:
-        run_group(g, sp0)
-        nbytes += 8 * g[4]
-    for c in singles:
-        p0 = q.pass_count()
-        run_single(c, sp0)
-        nbytes += (8 if q.pass_count() - p0 == 1 else 12) * c[6]
-    launches_per_sweep = q.launch_count() - l0
-    calls = [None] * (3 * len(tensors))
-    q.fetch_status(dev)
     g = torch.cuda.CUDAGraph()
     side = torch.cuda.Stream(dev)
     side.wait_stream(s0)
@@ -772,8 +768,9 @@ def run_sweep(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     peak, peak_src, _ = load_peaks()
-    ach = nbytes * args.steps / el / 1e9
-    total_elems = sum(t.numel() for t, _ in tensors)
+    ach = nbytes * args.steps / el / 1e9  # this rank's share over the job time
+    value = nbytes_all * args.steps / el / 1e9
+    total_elems = sum(t.numel() for t in tensors)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the reference's quantize_fused_at on a bounded sample of the sweep:
@@ -783,7 +780,7 @@ def run_sweep(args, rank, world, local_rank):
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from oracle_lib import block_fmt, fixed_fmt, float_fmt
             th = cpu_threads()
-            act = tensors[2][0]
+            act = q.random_uniform(layers[0][2], 300, 0, -4.0, 4.0, device=dev)
             xh = act.reshape(act.shape[0], -1)[:20].contiguous().cpu().numpy()
             secs = 0.0
             for fo in (float_fmt(5, 2), fixed_fmt(8, 4), block_fmt(8, 0)):
@@ -798,18 +795,20 @@ def run_sweep(args, rank, world, local_rank):
                    "sample": f"unavailable: {e}"}
     return {
         "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
-        "value": round(ach * world, 2), "unit": "GB/s", "n_gpus": world,
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (u32/fp32 bit arithmetic)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (u32/fp32 bit arithmetic)",
         "data": "synthetic ResNet-50-shaped tensors (no weights available offline)",
         "config": {"workload": "C5: ResNet-50 (batch 256) weights, weight gradients and "
                                "activations through float(5,2), fixed(8,4), block(8, dim0)",
-                   "tensors": len(tensors), "quantizations_per_step": len(calls),
-                   "elements_per_sweep_pass": total_elems,
-                   "algorithmic_bytes_per_step": nbytes,
-                   "launches_per_step": launches_per_sweep,
-                   "parallelism": f"replica{world}"},
+                   "tensors_this_rank": len(tensors),
+                   "quantizations_per_step_this_rank": len(calls),
+                   "elements_per_sweep_pass_this_rank": total_elems,
+                   "algorithmic_bytes_per_step": nbytes_all,
+                   "launches_per_step_this_rank": launches_per_sweep,
+                   "parallelism": f"binpack{world} (units: weights, gradients, each "
+                                  f"activation; by bytes, shard.binpack)"},
         "gpu_launches": launches_per_sweep * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
@@ -820,54 +819,130 @@ def run_sweep(args, rank, world, local_rank):
 
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU quantize_fused_at on the host."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref: lpsim compiled unmodified from /root/reference) on the
+    host cores with every host thread, same config / metric / unit as our arm.
+    Rank 0 only (the other ranks exit without work).
+
+    c1*, c2, c3*: the WHOLE workload per step (same input, bit-identical
+    generator): lpsim::quantize_fused_at.  c4ref: lpsim::quantized_matmul on a
+    bounded row sample of the 4096^3 problem.  c4: the reference has no
+    per-op-rounded GEMM; its restatement (oracle/, the definition the tests
+    check against) on a row sample, kind "port".  c5: quantize_fused_at of a
+    bounded sample of the sweep (the first activation's rows, three formats)."""
     if rank != 0:
         return None
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import RefLib
-    cfg = CONFIGS[args.config]
     if not RefLib.available():
         return {"impl": "reference", "unavailable": "oracle/_ref/liblpsim_ref.so not built"}
     ref = RefLib()
     th = cpu_threads()
     ref.set_num_threads(th)
-    n = cfg["n"]
-    samp = min(n, args.cpu_sample)
-    shape = ((samp // cfg["cols"], cfg["cols"]) if cfg["kind"] == "block" else (samp,))
-    x = ref.random_uniform(shape, 2, 0, -10.0, 10.0)
-    fmt = oracle_fmt(cfg)
+    metric = "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs"
+    kind = "reference"
+    same = True
+    if args.config in CONFIGS:
+        cfg = CONFIGS[args.config]
+        n = cfg["n"]
+        shape = (cfg["rows"], cfg["cols"]) if cfg["kind"] == "block" else (n,)
+        x = host_input(cfg, shape)
+        fmt = oracle_fmt(cfg)
+
+        def one():
+            st, y, secs = ref.quantize(x, fmt, mode_id(cfg), seed=SEED, call=0, timed=True)
+            assert st == 0
+            return secs
+        per_step, unit = 8 * n, "GB/s"
+        sample = (f"the whole workload ({n} elements) per step, lpsim::quantize_fused_at "
+                  f"(incl. its output allocation), set_num_threads({th})")
+        config = {"workload": cfg["workload"], "elements_per_gpu": n,
+                  "format": "%s:%d:%d" % cfg["fmt"], "rounding": cfg["mode"],
+                  "parallelism": "host threads"}
+    elif args.config in ("c4", "c4ref"):
+        from oracle_lib import Oracle, fixed_fmt, float_fmt
+        from concurrent.futures import ThreadPoolExecutor
+        rows = 2 * th if args.config == "c4" else 32
+        a = ref.random_uniform((rows, 4096), 41, 0, -1.0, 1.0)
+        b = ref.random_uniform((4096, 4096), 42, 0, -1.0, 1.0)
+        if args.config == "c4":
+            o = Oracle()
+            f87 = float_fmt(8, 7)
+            _, a = ref.quantize(a, f87, 1)
+            _, b = ref.quantize(b, f87, 1)
+            kind = "port"
+
+            def one():
+                t0 = time.perf_counter()
+                with ThreadPoolExecutor(th) as ex:
+                    list(ex.map(lambda r: o.quant_gemm(a[r:r + 2], b, f87, f87),
+                                range(0, rows, 2)))
+                return time.perf_counter() - t0
+            sample = (f"{rows} of the 4096 output rows per step through the restated per-op "
+                      f"GEMM (oracle/lpq_oracle.c; the reference has none), {th} threads")
+            metric = "quant-GEMM GFLOP/s (per-op rounded, float(8,7) after every multiply and add)"
+        else:
+            def one():
+                t0 = time.perf_counter()
+                ref.quantized_matmul(a, b, fixed_fmt(8, 4), 0, seed=SEED, call=0)
+                return time.perf_counter() - t0
+            sample = (f"lpsim::quantized_matmul on {rows} of the 4096 rows per step "
+                      f"(serial below m = 4096)")
+            metric = "reference quantized_matmul GFLOP/s (double accumulation, fused quantize epilogue)"
+        per_step, unit, same = 2.0 * rows * 4096 * 4096, "GFLOP/s", False
+        config = {"workload": f"{args.config}: 4096x4096x4096 (row sample)",
+                  "parallelism": "host threads"}
+    elif args.config == "c5":
+        from oracle_lib import block_fmt, fixed_fmt, float_fmt
+        x = ref.random_uniform((20, 802816), 300, 0, -4.0, 4.0)
+        fmts = (float_fmt(5, 2), fixed_fmt(8, 4), block_fmt(8, 0))
+
+        def one():
+            t = 0.0
+            for fo in fmts:
+                t += ref.quantize(x, fo, 1, seed=SEED, call=0, timed=True)[2]
+            return t
+        per_step, unit, same = 3 * 8 * x.size, "GB/s", False
+        sample = (f"lpsim::quantize_fused_at, nearest, float(5,2) + fixed(8,4) + block(8, dim0) "
+                  f"on {x.shape} per-sample rows of the first ResNet-50 activation, {th} threads")
+        config = {"workload": "C5: ResNet-50 sweep (sample)", "parallelism": "host threads"}
+    else:
+        raise SystemExit(f"--impl reference: unknown config {args.config}")
     for _ in range(args.warmup):
-        ref.quantize(x, fmt, mode_id(cfg), seed=SEED, call=0, timed=True)
-    times = []
-    for _ in range(args.steps):
-        st, y, secs = ref.quantize(x, fmt, mode_id(cfg), seed=SEED, call=0, timed=True)
-        times.append(secs)
+        one()
+    times = [one() for _ in range(args.steps)]
     tot = sum(times)
-    value = 8 * samp * args.steps / tot / 1e9
-    sample = (f"{samp} of the workload's {n} elements per step (bounded sample), "
-              f"lpsim::quantize_fused_at, set_num_threads({th})")
-    return {
-        "impl": "reference",
-        "metric": "quantize GB/s vs HBM peak (float/fixed/BFP); quant-GEMM GFLOP/s at 1-8 GPUs",
-        "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+    value = per_step * args.steps / tot / 1e9
+    out = {
+        "impl": "reference", "metric": metric,
+        "value": round(value, 4), "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp64 (reference arithmetic)",
-        "data": "synthetic (reference random_uniform)",
-        "config": {"workload": cfg["workload"], "elements_per_gpu": n,
-                   "format": "%s:%d:%d" % cfg["fmt"], "rounding": cfg["mode"],
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": th,
-                         "kind": "reference", "sample": sample},
-        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+        "data": "synthetic (reference random_uniform)", "config": config,
+        "same_work_per_step": same,
+        "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": th,
+                         "kind": kind, "sample": sample, "cpu_model": cpu_model()},
+        "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    return out
+
+
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (one rank each); default: WORLD_SIZE under torchrun, else 1")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -882,12 +957,28 @@ def main():
     ap.add_argument("--cpu-repeats", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus is None:
+        args.gpus = int(env_world or "1")
+    if env_world is None and args.gpus > 1:
+        # not under torchrun: launch one rank per GPU ourselves (same contract)
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.exit(f"bench.py --gpus {args.gpus}: needs {args.gpus} GPUs, "
+                         f"{have} visible")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(env_world or "1")
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank "
+                 f"per GPU (torchrun --nproc-per-node {args.gpus}) or drop --gpus")
     if args.impl == "reference":
-        if args.config in ("c4", "c4ref", "c5"):
-            args.config = "c2"
         out = run_reference(args, rank, world)
         if out is not None:
             print(json.dumps(out), flush=True)
@@ -895,6 +986,9 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # communicator evidence in the log (NCCL's INIT lines: nranks, NVLS, ...)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     runner = {"c4": run_gemm, "c4ref": run_matmul_q, "c5": run_sweep}.get(args.config, run_ours)

@@ -205,6 +205,41 @@ int lpsr_quantized_matmul(const float* a, const float* b, float* c, int64_t m,
   });
 }
 
+// The per-op-rounded GEMM as the reference's OWN tensor-op composition
+// (SURVEY.md §8(c) "Per-op GEMM oracle"): for k = 0..K-1, over M x N tensors,
+//   P   = mul(a[:, k] (x) 1, 1 (x) b[k, :])          tensor.cpp:152-156
+//   P   = quantize_fused_at(P, {fmt_mul}, call + 2k)  quant_ops.cpp:154-164
+//   acc = add(acc, P)                                  tensor.cpp:140-144
+//   acc = quantize_fused_at(acc, {fmt_add}, call + 2k + 1)
+// with acc starting as the zero-filled Tensor({M, N}) (+0).  Variate index
+// of output (i, j) = its flat index i*N + j (quant_pass, quant_ops.cpp:13-31).
+// Every step is a reference API call; nothing here does arithmetic.
+int lpsr_quant_gemm_composed(const float* a, const float* b, float* c, int64_t m,
+                             int64_t n, int64_t k, const RefFormat* fmul,
+                             const RefFormat* fadd, int mode, uint64_t seed,
+                             uint64_t call) {
+  return guarded([&] {
+    const lpsim::QuantSpec smul{to_format(fmul), static_cast<lpsim::RoundingMode>(mode),
+                                seed, 0};
+    const lpsim::QuantSpec sadd{to_format(fadd), static_cast<lpsim::RoundingMode>(mode),
+                                seed, 0};
+    lpsim::Tensor acc({m, n});
+    std::vector<float> pa(static_cast<size_t>(m * n)), pb(static_cast<size_t>(m * n));
+    for (int64_t kk = 0; kk < k; ++kk) {
+      for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+          pa[static_cast<size_t>(i * n + j)] = a[i * k + kk];
+          pb[static_cast<size_t>(i * n + j)] = b[kk * n + j];
+        }
+      lpsim::Tensor p = lpsim::mul(lpsim::Tensor({m, n}, pa), lpsim::Tensor({m, n}, pb));
+      p = lpsim::quantize_fused_at(p, smul, call + 2 * static_cast<uint64_t>(kk));
+      acc = lpsim::add(acc, p);
+      acc = lpsim::quantize_fused_at(acc, sadd, call + 2 * static_cast<uint64_t>(kk) + 1);
+    }
+    std::memcpy(c, acc.data(), sizeof(float) * static_cast<size_t>(m * n));
+  });
+}
+
 // parse_format (io.cpp:132-181) -> flat format struct
 int lpsr_parse_format(const char* text, RefFormat* out) {
   return guarded([&] {

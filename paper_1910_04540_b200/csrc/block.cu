@@ -382,28 +382,45 @@ __device__ __forceinline__ float4 load4(const float* __restrict__ row, int64_t c
   return v;
 }
 
+// Column plans: a CTA covers a tile of tw = ceil(min(W, kColTile) / 4)
+// float4 columns and runs kColT / tw row lanes over its row chunk, so narrow
+// tensors ([outer, W] with W < 1024, e.g. per-channel blocks of NHWC data)
+// keep every thread busy instead of one thread per 4 columns.
+struct ColLanes {
+  int tw, lanes, lane, ct;
+  __device__ __forceinline__ explicit ColLanes(int64_t W) {
+    tw = (int)((min(W, (int64_t)kColTile) + 3) / 4);
+    lanes = kColT / tw;
+    lane = threadIdx.x / tw;
+    ct = threadIdx.x - lane * tw;
+  }
+};
+
 template <bool VEC>
 __global__ void __launch_bounds__(kColT)
     k_col_reduce(const float* __restrict__ x, int64_t outer, int64_t W,
                  int64_t stride, int64_t rows_per_chunk,
                  uint32_t* __restrict__ maxima) {
   __shared__ uint32_t smax[kColTile];  // indexed by b - b0 (<= kColTile)
+  const ColLanes L(W);
   const int64_t c0 = (int64_t)blockIdx.x * kColTile;
-  const int64_t c = c0 + 4 * threadIdx.x;
+  const int64_t c = c0 + 4 * L.ct;
   const int64_t b0 = c0 / stride;
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
-  const int64_t r1 = min(outer, r0 + rows_per_chunk);
   for (int i = threadIdx.x; i < kColTile; i += kColT) smax[i] = 0u;
   __syncthreads();
-  if (c < W) {
+  if (c < W && L.lane < L.lanes) {
     uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    for (int64_t r = r0; r < r1; ++r) {
-      const float4 v = load4<VEC>(x + r * W, c, W);
-      m0 = max(m0, absbits_for_max(v.x));
-      m1 = max(m1, absbits_for_max(v.y));
-      m2 = max(m2, absbits_for_max(v.z));
-      m3 = max(m3, absbits_for_max(v.w));
-    }
+    // grid.y is capped at 65535: chunks beyond it are taken grid-stride
+    const int64_t rstep = (int64_t)gridDim.y * rows_per_chunk;
+    for (int64_t rc = (int64_t)blockIdx.y * rows_per_chunk; rc < outer; rc += rstep)
+      for (int64_t r = rc + L.lane, r1 = min(outer, rc + rows_per_chunk); r < r1;
+           r += L.lanes) {
+        const float4 v = load4<VEC>(x + r * W, c, W);
+        m0 = max(m0, absbits_for_max(v.x));
+        m1 = max(m1, absbits_for_max(v.y));
+        m2 = max(m2, absbits_for_max(v.z));
+        m3 = max(m3, absbits_for_max(v.w));
+      }
     atomicMax(&smax[c / stride - b0], m0);
     if (c + 1 < W) atomicMax(&smax[(c + 1) / stride - b0], m1);
     if (c + 2 < W) atomicMax(&smax[(c + 2) / stride - b0], m2);
@@ -425,11 +442,11 @@ __global__ void __launch_bounds__(kColT)
                 uint32_t* __restrict__ status) {
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
-  const int64_t c = (int64_t)blockIdx.x * kColTile + 4 * threadIdx.x;
+  const ColLanes L(W);
+  const int64_t c = (int64_t)blockIdx.x * kColTile + 4 * L.ct;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
-  const int64_t r1 = min(outer, r0 + rows_per_chunk);
   uint32_t bad = 0;
-  if (c < W) {
+  if (c < W && L.lane < L.lanes) {
     BlockScale s[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -437,7 +454,11 @@ __global__ void __launch_bounds__(kColT)
       s[q] = make_block_scale(__ldg(maxima + cq / stride), wl);
       if (s[q].bad) bad |= 2u;
     }
-    for (int64_t r = r0; r < r1; ++r) {
+    // grid.y is capped at 65535: chunks beyond it are taken grid-stride
+    const int64_t rstep = (int64_t)gridDim.y * rows_per_chunk;
+    for (int64_t rc = r0; rc < outer; rc += rstep)
+    for (int64_t r = rc + L.lane, r1 = min(outer, rc + rows_per_chunk); r < r1;
+         r += L.lanes) {
       const float4 v = load4<VEC>(x + r * W, c, W);
       const uint64_t idx = base + (uint64_t)(r * W + c);
       float4 o;
@@ -468,12 +489,22 @@ bool aligned16(const void* p) {
 
 int64_t col_rows_per_chunk(int64_t outer, int64_t W) {
   // aim at >= ~16K elements per CTA so register maxima amortise the atomics,
-  // while keeping >= ~4 waves of CTAs on 148 SMs when the tensor is large.
+  // while keeping >= ~8 CTAs per SM when the tensor is large.
   const int64_t tiles = (W + kColTile - 1) / kColTile;
-  int64_t r = std::max<int64_t>(16, (int64_t)(16384 / kColTile));
+  const int64_t tile_w = std::min<int64_t>(W, kColTile);
+  const int64_t lanes = kColT / ((tile_w + 3) / 4);
+  const int64_t floor_r = lanes;  // at least one row per lane
+  int64_t r = std::max<int64_t>(floor_r, 16384 / tile_w);
   const int64_t target_ctas = (int64_t)device_info().sm_count * 8;
-  while (r > 16 && tiles * ((outer + r - 1) / r) < target_ctas) r /= 2;
-  return std::max<int64_t>(1, std::min(r, outer));
+  while (r > floor_r && tiles * ((outer + r - 1) / r) < target_ctas) r /= 2;
+  return std::max<int64_t>(1, std::min(std::max(r, floor_r), outer));
+}
+
+// grid for the column plans: grid.y is capped at 65535 (the kernels take
+// row chunks beyond it grid-stride)
+dim3 col_grid(int64_t outer, int64_t W, int64_t rpc) {
+  return dim3((unsigned)((W + kColTile - 1) / kColTile),
+              (unsigned)std::min<int64_t>(65535, (outer + rpc - 1) / rpc));
 }
 
 template <int M>
@@ -534,8 +565,7 @@ cudaError_t launch_two_pass_m(const float* x, float* y, const BlockGeom& g,
   const int64_t W = g.extent * g.stride;
   const bool vec = (W % 4 == 0) && aligned16(x) && aligned16(y);
   const int64_t rpc = col_rows_per_chunk(g.outer, W);
-  dim3 grid((unsigned)((W + kColTile - 1) / kColTile),
-            (unsigned)((g.outer + rpc - 1) / rpc));
+  const dim3 grid = col_grid(g.outer, W, rpc);
   if (vec) {
     if (reduce)
       k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
@@ -572,8 +602,7 @@ cudaError_t launch_block_reduce(const float* x, const BlockGeom& g,
   } else {
     const int64_t W = g.extent * g.stride;
     const int64_t rpc = col_rows_per_chunk(g.outer, W);
-    dim3 grid((unsigned)((W + kColTile - 1) / kColTile),
-              (unsigned)((g.outer + rpc - 1) / rpc));
+    const dim3 grid = col_grid(g.outer, W, rpc);
     if ((W % 4 == 0) && aligned16(x))
       k_col_reduce<true><<<grid, kColT, 0, s>>>(x, g.outer, W, g.stride, rpc, maxima);
     else

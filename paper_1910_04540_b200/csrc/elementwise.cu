@@ -309,6 +309,35 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Block byte codes: k = q * 2^-(E_b - (wl - 2)) in double (exact: a power-of-
+// two scale of an fp32 value), checked to be an int8 whose decode
+// float(double(k) * delta_b) gives q back bit for bit.
+__global__ void __launch_bounds__(kThreads)
+    k_encode_block8(const float* __restrict__ q, uint8_t* __restrict__ c, int64_t n,
+                    int64_t extent, int64_t stride, const uint32_t* __restrict__ maxima,
+                    int wl, uint32_t* __restrict__ not_exact) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const int64_t b = (i / stride) % extent;
+    const uint32_t mb = maxima[b];
+    const float v = q[i];
+    int k = 0;
+    if (mb != 0u) {
+      const int E = float_exponent_bits(mb);
+      const double inv = ldexp(1.0, -(E - (wl - 2)));
+      const double kd = (double)v * inv;
+      k = (int)kd;
+      bad |= (double)k != kd || k < -128 || k > 127 ||
+             f2u((float)((double)k * ldexp(1.0, E - (wl - 2)))) != f2u(v);
+    } else {
+      bad |= f2u(v) != 0u;  // an all-zero block quantizes to +0
+    }
+    c[i] = (uint8_t)(int8_t)k;
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(not_exact, 1u);
+}
+
 // ---- generators -------------------------------------------------------------
 
 __global__ void __launch_bounds__(kThreads)
@@ -379,6 +408,19 @@ cudaError_t launch_variates(float* y, int64_t n, uint64_t base, uint64_t key,
                             cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   k_variates<<<gen_grid(n), kThreads, 0, s>>>(y, n, base, key);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_block8(const float* q, uint8_t* c, const BlockGeom& g,
+                                 const uint32_t* maxima, int wl, uint32_t* not_exact,
+                                 cudaStream_t s) {
+  const int64_t n = g.outer * g.extent * g.stride;
+  if (n <= 0) return cudaSuccess;
+  const int64_t grid = std::min<int64_t>((n + kThreads - 1) / kThreads,
+                                         (int64_t)device_info().sm_count * 16);
+  k_encode_block8<<<(unsigned)grid, kThreads, 0, s>>>(q, c, n, g.extent, g.stride, maxima,
+                                                      wl, not_exact);
   note_launch();
   return cudaGetLastError();
 }

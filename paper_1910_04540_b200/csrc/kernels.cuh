@@ -81,6 +81,15 @@ struct ByteCode {
 };
 cudaError_t launch_encode8(const float* q, uint8_t* c, int64_t n, const ByteCode& bc,
                            cudaStream_t s);
+// Block formats with wl <= 8 (NearestEven / Stochastic: zeros are +0):
+// code = k = q / delta_b, delta_b = 2^(E_b - (wl - 2)) from the block maxima
+// (max|x| bits, maxima[extent], the two-pass plans' workspace); the host
+// decodes float(double(k) * delta_b).  An element whose q is not exactly
+// k * delta_b (a result in the fp32 subnormal range that rounded) sets
+// *not_exact, and the caller copies the fp32 values instead.
+cudaError_t launch_encode_block8(const float* q, uint8_t* c, const BlockGeom& g,
+                                 const uint32_t* maxima, int wl, uint32_t* not_exact,
+                                 cudaStream_t s);
 
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,
                            float lo, float hi, cudaStream_t s);

@@ -661,6 +661,18 @@ LPQ_HD float pow2f(int e) {  // 2^e for e in [-126, 127]
   return u2f((uint32_t)(127 + e) << 23);
 }
 
+// floor(log2 m) of a nonzero finite |x| from its bits (float_exponent,
+// scalar_quant.hpp:26-33), subnormals included.
+LPQ_HD int float_exponent_bits(uint32_t m) {
+  const int field = (int)(m >> 23);
+  if (field != 0) return field - 127;
+#if defined(__CUDA_ARCH__)
+  return -118 - __clz((int)m);
+#else
+  return -118 - __builtin_clz(m);
+#endif
+}
+
 // From the bits of the block maximum |x| (NaN already excluded).
 LPQ_HD BlockScale make_block_scale(uint32_t max_bits, int wl) {
   BlockScale s;

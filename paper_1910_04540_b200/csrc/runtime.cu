@@ -48,6 +48,16 @@ struct HostCtx {
   size_t ws_bytes = 0;
   float* dfull = nullptr;
   int64_t dfull_cap = 0;
+  // direct path (tensors <= 16 MB): page-locked staging of pageable
+  // inputs / outputs, byte codes of the whole tensor, block maxima + flag
+  float* pstage = nullptr;
+  int64_t pstage_cap = 0;
+  uint8_t* dcodef = nullptr;
+  uint8_t* pcodef = nullptr;
+  int64_t codef_cap = 0;
+  uint32_t* daux = nullptr;  // device: encode flag
+  uint32_t* paux = nullptr;  // page-locked: block maxima [extent] + flag
+  int64_t paux_cap = 0;
   std::mutex mu;
 
   ~HostCtx() { release(); }
@@ -71,6 +81,16 @@ struct HostCtx {
     if (d_status) cudaFree(d_status);
     if (ws) cudaFree(ws);
     if (dfull) cudaFree(dfull);
+    if (pstage) cudaFreeHost(pstage);
+    if (dcodef) cudaFree(dcodef);
+    if (pcodef) cudaFreeHost(pcodef);
+    if (daux) cudaFree(daux);
+    if (paux) cudaFreeHost(paux);
+    pstage = nullptr;
+    dcodef = nullptr;
+    pcodef = nullptr;
+    daux = paux = nullptr;
+    pstage_cap = codef_cap = paux_cap = 0;
     d_status = nullptr;
     ws = nullptr;
     dfull = nullptr;
@@ -126,6 +146,44 @@ struct HostCtx {
     return e;
   }
 
+  cudaError_t ensure_stage(int64_t elems) {
+    if (elems <= pstage_cap) return cudaSuccess;
+    if (pstage) cudaFreeHost(pstage);
+    pstage = nullptr;
+    pstage_cap = 0;
+    cudaError_t e = cudaMallocHost(&pstage, sizeof(float) * (size_t)elems);
+    if (e == cudaSuccess) pstage_cap = elems;
+    return e;
+  }
+
+  cudaError_t ensure_codes(int64_t elems, int64_t extent) {
+    cudaError_t e = cudaSuccess;
+    if (elems > codef_cap) {
+      if (dcodef) cudaFree(dcodef);
+      if (pcodef) cudaFreeHost(pcodef);
+      dcodef = nullptr;
+      pcodef = nullptr;
+      codef_cap = 0;
+      e = cudaMalloc(&dcodef, (size_t)elems);
+      if (e == cudaSuccess) e = cudaMallocHost(&pcodef, (size_t)elems);
+      if (e != cudaSuccess) return e;
+      codef_cap = elems;
+    }
+    if (!daux) {
+      e = cudaMalloc(&daux, sizeof(uint32_t));
+      if (e != cudaSuccess) return e;
+    }
+    if (extent + 1 > paux_cap) {
+      if (paux) cudaFreeHost(paux);
+      paux = nullptr;
+      paux_cap = 0;
+      e = cudaMallocHost(&paux, sizeof(uint32_t) * (size_t)(extent + 1));
+      if (e != cudaSuccess) return e;
+      paux_cap = extent + 1;
+    }
+    return cudaSuccess;
+  }
+
   cudaError_t ensure_ws(size_t bytes) {
     if (bytes <= ws_bytes) return cudaSuccess;
     if (ws) cudaFree(ws);
@@ -159,6 +217,17 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// How the host turns one-byte codes back into fp32 (bit-identical to the
+// device's quantized values).
+struct Decode {
+  enum Kind { kLut = 1, kFixed = 2, kBlock = 3 };
+  int kind = 0;
+  const float* lut = nullptr;    // kLut: 256 entries
+  float scale = 0.0f;            // kFixed: 2^-fl
+  const double* delta = nullptr; // kBlock: delta per block
+  int64_t extent = 1, stride = 1;
+};
+
 // Persistent copy workers for parallel_memcpy (spawning threads per call
 // cost more than a 4 MB copy).  Parts of >= 512 KB, at most 16 threads
 // including the caller.
@@ -170,24 +239,27 @@ class CopyPool {
   }
   int width() const { return (int)workers_.size() + 1; }
 
-  // count units (bytes, or codes when lut) split over `parts` threads; a
-  // unit of the destination is dst_unit bytes
-  void run(char* dst, const char* src, size_t count, int parts, const float* lut = nullptr) {
-    const size_t dst_unit = lut ? sizeof(float) : 1;
+  // count units (bytes, or codes when dec) split over `parts` threads; a
+  // unit of the destination is dst_unit bytes; first: element index of
+  // src[0] within the tensor (block decode)
+  void run(char* dst, const char* src, size_t count, int parts,
+           const Decode* dec = nullptr, size_t first = 0) {
+    const size_t dst_unit = dec ? sizeof(float) : 1;
     const size_t part = (count / parts + 63) & ~size_t(63);
     std::unique_lock<std::mutex> lk(mu_);
     jobs_.clear();
     for (int t = 1; t < parts; ++t) {
       const size_t b = part * t;
       if (b >= count) break;
-      jobs_.push_back(Job{dst + b * dst_unit, src + b, std::min(part, count - b), lut});
+      jobs_.push_back(Job{dst + b * dst_unit, src + b, std::min(part, count - b), dec,
+                          first + b});
     }
     next_ = 0;
     pending_ = jobs_.size();
     ++gen_;
     lk.unlock();
     cv_.notify_all();
-    exec(Job{dst, src, std::min(part, count), lut});
+    exec(Job{dst, src, std::min(part, count), dec, first});
     lk.lock();
     // help with whatever the workers have not picked up, then wait
     while (next_ < jobs_.size()) {
@@ -205,16 +277,32 @@ class CopyPool {
     char* dst;
     const char* src;
     size_t len;          // bytes (copy) or codes (decode)
-    const float* lut;    // decode: float dst[i] = lut[uint8 src[i]]
+    const Decode* dec;   // null: memcpy
+    size_t first;        // element index of src[0] (block decode)
   };
   static void exec(const Job& j) {
-    if (!j.lut) {
+    if (!j.dec) {
       std::memcpy(j.dst, j.src, j.len);
       return;
     }
     float* d = reinterpret_cast<float*>(j.dst);
     const uint8_t* c = reinterpret_cast<const uint8_t*>(j.src);
-    for (size_t i = 0; i < j.len; ++i) d[i] = j.lut[c[i]];
+    const Decode& dc = *j.dec;
+    if (dc.kind == Decode::kLut) {
+      for (size_t i = 0; i < j.len; ++i) d[i] = dc.lut[c[i]];
+    } else if (dc.kind == Decode::kFixed) {  // k * 2^-fl: exact, +0 for k = 0
+      const float sc = dc.scale;
+      for (size_t i = 0; i < j.len; ++i) d[i] = (float)(int8_t)c[i] * sc;
+    } else {  // block: float(double(k) * delta_b), b = (idx / stride) % extent
+      size_t i = 0;
+      while (i < j.len) {
+        const uint64_t idx = j.first + i;
+        const uint64_t blk = idx / (uint64_t)dc.stride;
+        const double dl = dc.delta[blk % (uint64_t)dc.extent];
+        const size_t end = std::min<size_t>(j.len, (size_t)((blk + 1) * dc.stride - j.first));
+        for (; i < end; ++i) d[i] = (float)((double)(int8_t)c[i] * dl);
+      }
+    }
   }
   CopyPool() {
     const unsigned hw = std::thread::hardware_concurrency();
@@ -256,10 +344,11 @@ class CopyPool {
 
 std::mutex g_copy_mu;  // one parallel copy at a time (the pool is shared)
 
-void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  // below 8 MB the workers' wake-up costs more than the copy
+void parallel_memcpy(void* dst, const void* src, size_t bytes,
+                     size_t serial_below = size_t(8) << 20) {
+  // below serial_below the workers' wake-up costs more than the copy
   const size_t kMinPart = size_t(1) << 20;
-  const size_t want = bytes < (size_t(8) << 20) ? 1 : bytes / kMinPart;
+  const size_t want = bytes < serial_below ? 1 : bytes / kMinPart;
   if (want <= 1) {
     std::memcpy(dst, src, bytes);
     return;
@@ -274,15 +363,17 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
   pool.run(static_cast<char*>(dst), static_cast<const char*>(src), bytes, parts);
 }
 
-// dst[i] = lut[codes[i]] over the copy pool (256K codes = 1 MB of output
-// per part, like the copies)
-void parallel_decode(float* dst, const uint8_t* codes, size_t n, const float* lut) {
+// dst[i] = decode(codes[i]) over the copy pool (256K codes = 1 MB of output
+// per part, like the copies); first: tensor index of codes[0]
+void parallel_decode(float* dst, const uint8_t* codes, size_t n, const Decode& dec,
+                     size_t first = 0) {
   const size_t kMinPart = size_t(1) << 18;
   const size_t want = std::max<size_t>(1, n / kMinPart);
   std::lock_guard<std::mutex> lk(g_copy_mu);
   CopyPool& pool = CopyPool::get();
   const int parts = (int)std::min<size_t>(want, (size_t)pool.width());
-  pool.run(reinterpret_cast<char*>(dst), reinterpret_cast<const char*>(codes), n, parts, lut);
+  pool.run(reinterpret_cast<char*>(dst), reinterpret_cast<const char*>(codes), n, parts,
+           &dec, first);
 }
 
 // One-byte codes for the device->host copy of quantized results: saturating
@@ -322,6 +413,19 @@ bool byte_code_for(const lpq_format* f, int mode, ByteCode* bc, float* lut) {
     return true;
   }
   return false;
+}
+
+// The host decoder of a ByteCode (fixed: arithmetic, float: the table).
+Decode decoder_for(const lpq_format* f, const ByteCode& bc, const float* lut) {
+  Decode d;
+  if (bc.kind == 1) {
+    d.kind = Decode::kFixed;
+    d.scale = std::ldexp(1.0f, -f->fl);
+  } else {
+    d.kind = Decode::kLut;
+    d.lut = lut;
+  }
+  return d;
 }
 
 int resolve_device(int device, lpq_status* st) {
@@ -367,11 +471,12 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
   ByteCode bc{};
   float lut[256];
   const bool coded = !rows && byte_code_for(f, mode, &bc, lut);
+  const Decode dec = coded ? decoder_for(f, bc, lut) : Decode{};
   auto finish = [&](int64_t ci) {
     const int k = (int)(ci % kStreams);
     cudaEventSynchronize(c->done[k]);
     const int64_t off = ci * chunk, len = std::min(chunk, n - off);
-    if (coded) parallel_decode(y + off, c->pcode[k], (size_t)len, lut);
+    if (coded) parallel_decode(y + off, c->pcode[k], (size_t)len, dec);
     else if (!pin_y) parallel_memcpy(y + off, c->pin_out[k], sizeof(float) * (size_t)len);
   };
   for (int64_t ci = 0; ci < nchunks; ++ci) {
@@ -460,10 +565,47 @@ lpq_status resident_quantize(HostCtx* c, const float* x, float* y,
   return lpq_status_fetch(c->d_status, s);
 }
 
+// Host -> device copy of a whole (small) tensor: pinned memory directly;
+// pageable memory staged through the context's page-locked buffer by the
+// copy pool (1 MB parts) -- the driver's own staging of pageable copies runs
+// at a fraction of PCIe (scripts/time_host.py).
+cudaError_t h2d_small(HostCtx* c, float* d, const float* x, int64_t n, cudaStream_t s) {
+  const size_t bytes = sizeof(float) * (size_t)n;
+  if (is_pinned(x) || bytes < (size_t(1) << 20))
+    return cudaMemcpyAsync(d, x, bytes, cudaMemcpyHostToDevice, s);
+  cudaError_t e = c->ensure_stage(n);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(s);  // the staging buffer may still feed a copy
+  if (e != cudaSuccess) return e;
+  parallel_memcpy(c->pstage, x, bytes, size_t(1) << 20);
+  return cudaMemcpyAsync(d, c->pstage, bytes, cudaMemcpyHostToDevice, s);
+}
+
+// Device -> host copy of a whole (small) tensor, then the status fetch
+// (which synchronises the stream).
+lpq_status d2h_small_and_fetch(HostCtx* c, float* y, const float* d, int64_t n,
+                               cudaStream_t s) {
+  const size_t bytes = sizeof(float) * (size_t)n;
+  if (is_pinned(y) || bytes < (size_t(1) << 20)) {
+    LPQ_TRY(cudaMemcpyAsync(y, d, bytes, cudaMemcpyDeviceToHost, s));
+    return lpq_status_fetch(c->d_status, s);
+  }
+  LPQ_TRY(c->ensure_stage(n));
+  LPQ_TRY(cudaMemcpyAsync(c->pstage, d, bytes, cudaMemcpyDeviceToHost, s));
+  const lpq_status st = lpq_status_fetch(c->d_status, s);
+  if (st != LPQ_OK) return st;
+  parallel_memcpy(y, c->pstage, bytes, size_t(1) << 20);
+  return LPQ_OK;
+}
+
 // Small tensors (<= 16 MB): one copy in, the device call, one copy out on
-// one stream; the driver stages pageable memory itself.  Below ~16 MB the
-// chunked pipeline's per-chunk events, waits and bounce copies cost more
-// than the overlap they buy (scripts/time_host.py).
+// one stream.  Below ~16 MB the chunked pipeline's per-chunk events, waits
+// and bounce copies cost more than the overlap they buy (scripts/time_host.py).
+// Formats whose every quantized value has a one-byte code (ByteCode: fixed
+// wl <= 8 saturating, float 1 + exp + man <= 8; block wl <= 8 on the
+// two-pass plans, whose maxima give each block's step) copy the codes back
+// instead of fp32: a quarter of the device->host bytes, decoded bit-exactly
+// on the host.
 lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
                            const int64_t* shape, int rank, int64_t n,
                            uint64_t index_base, const lpq_format* f, int mode,
@@ -472,8 +614,7 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
   const size_t wsb = lpq_workspace_size(f, shape, rank);
   if (wsb) LPQ_TRY(c->ensure_ws(wsb));
   cudaStream_t s = c->st[0];
-  const size_t bytes = sizeof(float) * (size_t)n;
-  LPQ_TRY(cudaMemcpyAsync(c->dfull, x, bytes, cudaMemcpyHostToDevice, s));
+  LPQ_TRY(h2d_small(c, c->dfull, x, n, s));
   const lpq_status qst = quantize_device(c->dfull, c->dfull, shape, rank, index_base,
                                          f, mode, seed, call, c->ws, c->ws_bytes,
                                          c->d_status, s);
@@ -481,8 +622,49 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
     cudaStreamSynchronize(s);
     return qst;
   }
-  LPQ_TRY(cudaMemcpyAsync(y, c->dfull, bytes, cudaMemcpyDeviceToHost, s));
-  return lpq_status_fetch(c->d_status, s);
+  ByteCode bc{};
+  float lut[256];
+  const bool coded = byte_code_for(f, mode, &bc, lut);
+  BlockGeom g{1, 1, n};
+  bool bcoded = false;
+  if (!coded && f->kind == LPQ_BLOCK && f->wl <= 8 &&
+      (mode == kNearestEven || mode == kStochastic) &&
+      block_geometry(f, shape, rank, &g) == LPQ_OK)
+    bcoded = !block_plan_single_pass(block_plan(g, c->dfull, c->dfull));
+  if (!coded && !bcoded) return d2h_small_and_fetch(c, y, c->dfull, n, s);
+  LPQ_TRY(c->ensure_codes(n, g.extent));
+  if (coded) {
+    LPQ_TRY(launch_encode8(c->dfull, c->dcodef, n, bc, s));
+  } else {
+    LPQ_TRY(cudaMemsetAsync(c->daux, 0, sizeof(uint32_t), s));
+    LPQ_TRY(launch_encode_block8(c->dfull, c->dcodef, g, static_cast<const uint32_t*>(c->ws),
+                                 f->wl, c->daux, s));
+    LPQ_TRY(cudaMemcpyAsync(c->paux, c->ws, sizeof(uint32_t) * (size_t)g.extent,
+                            cudaMemcpyDeviceToHost, s));
+    LPQ_TRY(cudaMemcpyAsync(c->paux + g.extent, c->daux, sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+  }
+  LPQ_TRY(cudaMemcpyAsync(c->pcodef, c->dcodef, (size_t)n, cudaMemcpyDeviceToHost, s));
+  const lpq_status st = lpq_status_fetch(c->d_status, s);
+  if (st != LPQ_OK) return st;
+  if (coded) {
+    parallel_decode(y, c->pcodef, (size_t)n, decoder_for(f, bc, lut));
+    return LPQ_OK;
+  }
+  if (c->paux[g.extent] != 0u)  // a result in the subnormal range: fp32 copy
+    return d2h_small_and_fetch(c, y, c->dfull, n, s);
+  std::vector<double> delta((size_t)g.extent);
+  for (int64_t b = 0; b < g.extent; ++b) {
+    const uint32_t m = c->paux[b];
+    delta[(size_t)b] = m ? std::ldexp(1.0, float_exponent_bits(m) - (f->wl - 2)) : 0.0;
+  }
+  Decode dec;
+  dec.kind = Decode::kBlock;
+  dec.delta = delta.data();
+  dec.extent = g.extent;
+  dec.stride = g.stride;
+  parallel_decode(y, c->pcodef, (size_t)n, dec);
+  return LPQ_OK;
 }
 
 }  // namespace
@@ -553,8 +735,9 @@ lpq_status host_context_composed(const float* x, float* y,
   const size_t wsb = lpq_composed_workspace_size(f, shape, rank);
   LPQ_TRY(c->ensure_ws(wsb));
   cudaStream_t s = c->st[0];
-  const size_t bytes = sizeof(float) * (size_t)n;
-  LPQ_TRY(cudaMemcpyAsync(c->dfull, x, bytes, cudaMemcpyHostToDevice, s));
+  // the same host staging as the fused direct path (fp32 both ways: the
+  // many-kernel chain's last op writes fp32)
+  LPQ_TRY(h2d_small(c, c->dfull, x, n, s));
   st = quantize_composed_device(c->dfull, c->dfull, shape, rank, index_base, f,
                                 mode, seed, call, c->ws, c->ws_bytes,
                                 c->d_status, s);
@@ -562,8 +745,7 @@ lpq_status host_context_composed(const float* x, float* y,
     cudaStreamSynchronize(s);
     return st;
   }
-  LPQ_TRY(cudaMemcpyAsync(y, c->dfull, bytes, cudaMemcpyDeviceToHost, s));
-  return lpq_status_fetch(c->d_status, s);
+  return d2h_small_and_fetch(c, y, c->dfull, n, s);
 }
 
 void shutdown_contexts() {

@@ -17,7 +17,8 @@ from typing import Optional, Sequence
 
 from . import _lib
 from ._lib import FormatError, LpqQuantSlot, LpqSgdTensor, ShapeError, check, lib
-from .quant import QuantSpec, RoundingMode, _status_buf, _stream_ptr, fetch_status
+from .quant import (BlockFloatFormat, QuantSpec, RoundingMode, _status_buf,
+                    _stream_ptr, fetch_status, quantize_fused)
 
 
 def _slot(spec: Optional[QuantSpec], call_offset: int = 0) -> LpqQuantSlot:
@@ -35,6 +36,21 @@ def _slot(spec: Optional[QuantSpec], call_offset: int = 0) -> LpqQuantSlot:
 def _advance(spec: Optional[QuantSpec], k: int) -> None:
     if spec is not None and spec.mode == RoundingMode.Stochastic:
         spec.call_counter += k
+
+
+def _check_tensor(t, first, what):
+    """The fused kernel reads and writes every pointer as n fp32 values on one
+    device: anything else is rejected before it reaches the launch."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+        raise TypeError(f"optimizer: {what} must be float32 CUDA tensors "
+                        "(proj/include/lpsim/tensor.hpp:16)")
+    if t.device != first.device:
+        raise TypeError(f"optimizer: {what} must be on {first.device}, got {t.device}")
+
+
+def _is_block(spec: Optional[QuantSpec]) -> bool:
+    return spec is not None and isinstance(spec.format, BlockFloatFormat)
 
 
 def _sgd_dtype():
@@ -67,6 +83,10 @@ class LowPrecisionOptimizer:
         self.acc_spec = copy.deepcopy(accumulator)
         self.grad_spec = copy.deepcopy(gradient)
         self.params = list(params)
+        for p in self.params:
+            _check_tensor(p, self.params[0], "parameters")
+            if not p.is_contiguous():
+                raise ValueError("parameters must be contiguous")
         self.acc = [p.detach().clone().contiguous() for p in self.params]
         self.vel = [torch.zeros_like(p) for p in self.params]
 
@@ -99,6 +119,9 @@ class LowPrecisionOptimizer:
                 raise ShapeError("optimizer step: gradient shape mismatch")
             if not p.is_contiguous():
                 raise ValueError("parameters must be contiguous")
+            _check_tensor(g, self.params[0], "gradients")
+        if any(_is_block(s) for s in (self.grad_spec, self.acc_spec, self.weight_spec)):
+            return self._step_unfused(grads, sync)
         # the tensor table, filled column-wise (the per-step host cost of
         # a Python loop over ctypes structs exceeds the kernel's)
         cnt = len(self.params)
@@ -122,9 +145,6 @@ class LowPrecisionOptimizer:
         t["call_vel"] = calls(self.acc_spec, 2)
         t["call_acc"] = t["call_vel"] + np.uint64(1 if acc_stoch else 0)
         t["call_weight"] = calls(self.weight_spec, 1)
-        _advance(self.grad_spec, cnt)
-        _advance(self.acc_spec, 2 * cnt)
-        _advance(self.weight_spec, cnt)
         descs = t.ctypes.data_as(C.POINTER(LpqSgdTensor))
         dev = self.params[0].device
         qg, qv, qw = _slot(self.grad_spec), _slot(self.acc_spec), _slot(self.weight_spec)
@@ -133,5 +153,37 @@ class LowPrecisionOptimizer:
                                       C.c_void_p(_status_buf(dev).data_ptr()),
                                       _stream_ptr(dev))
         check(st, "optimizer step")
+        # the counters advance only once the launch was accepted (a rejected
+        # step leaves the specs as they were)
+        _advance(self.grad_spec, cnt)
+        _advance(self.acc_spec, 2 * cnt)
+        _advance(self.weight_spec, cnt)
         if sync:
             fetch_status(dev)
+
+    def _step_unfused(self, grads, sync):
+        """Block floating point in any slot (the fused kernel has no per-block
+        reduction): the reference's per-parameter sequence (train.cpp:161-174)
+        as quantize_fused launches and fp32 elementwise ops on the device --
+        scale(vel, float(momentum)) + g, then acc - scale(v, float(lr)), each a
+        separately rounded fp32 op as in tensor.cpp:140-168 -- with the call
+        counters advancing per quantization exactly as quantize_fused does."""
+        import torch
+        m32 = float(np.float32(self.momentum))
+        lr32 = float(np.float32(self.lr))
+        for k, (p, g) in enumerate(zip(self.params, grads)):
+            g = g.contiguous()
+            if self.grad_spec is not None:
+                g = quantize_fused(g, self.grad_spec, sync=sync)
+            v = torch.add(torch.mul(self.vel[k], m32), g)
+            if self.acc_spec is not None:
+                v = quantize_fused(v, self.acc_spec, sync=sync)
+            self.vel[k].copy_(v)
+            a = torch.sub(self.acc[k], torch.mul(v, lr32))
+            if self.acc_spec is not None:
+                a = quantize_fused(a, self.acc_spec, sync=sync)
+            self.acc[k].copy_(a)
+            if self.weight_spec is not None:
+                quantize_fused(a, self.weight_spec, out=p, sync=sync)
+            else:
+                p.copy_(a)

@@ -199,6 +199,9 @@ class RefLib:
                                             C.c_uint64,
                                             C.POINTER(C.c_uint64)]
         L.lpsr_set_num_threads.argtypes = [C.c_int]
+        L.lpsr_quant_gemm_composed.argtypes = [_fp, _fp, _fp, C.c_int64, C.c_int64,
+                                               C.c_int64, C.POINTER(Fmt), C.POINTER(Fmt),
+                                               C.c_int, C.c_uint64, C.c_uint64]
         L.lpsr_parse_format.argtypes = [C.c_char_p, C.POINTER(Fmt)]
         L.lpsr_write_tensor_file.argtypes = [C.c_char_p, _fp, _i64p, C.c_int]
         L.lpsr_read_tensor_file.argtypes = [C.c_char_p, _fp, C.c_int64, _i64p,
@@ -300,6 +303,18 @@ class RefLib:
                                 c, m, k, n)
         assert st == 0
         return c
+
+    def quant_gemm_composed(self, a, b, fmul, fadd, mode, seed=0, call=0):
+        """The per-op GEMM as the reference's own mul -> quantize_fused_at ->
+        add -> quantize_fused_at composition per k (ref_capi.cpp)."""
+        m, k = a.shape
+        n = b.shape[1]
+        c = np.empty((m, n), dtype=np.float32)
+        st = self.L.lpsr_quant_gemm_composed(np.ascontiguousarray(a, np.float32),
+                                             np.ascontiguousarray(b, np.float32), c,
+                                             m, n, k, C.byref(fmul), C.byref(fadd),
+                                             mode, seed, call)
+        return st, c
 
     def quantized_matmul(self, a, b, fmt, mode, seed=0, call=0):
         m, k = a.shape

@@ -42,6 +42,7 @@ def test_reference_acceptance_criteria_on_the_dropin():
     for n in range(1, 8 + 1):
         tagged = [l for l in lines if f"criterion {n}:" in l]
         assert tagged, f"criterion {n} missing"
-        if n == 7:
-            continue  # host-API timing ratio, reported
+        # criterion 7 (fused <= 0.7 x composed through the host API at 2^20,
+        # acceptance.cpp:340-377) included: the fused direct host path copies
+        # one-byte codes back (runtime.cu direct_quantize)
         assert tagged[0].startswith("PASS"), tagged[0]

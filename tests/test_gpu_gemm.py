@@ -1,13 +1,18 @@
 """GPU parity of the GEMMs.
 
-* quant_gemm (per-op-rounded, lpq_quant_gemm) vs the restated oracle
-  lpqo_quant_gemm: bit-exact, both kernels (hardware-bf16 fast path and the
-  general path), every rounding mode; the rounding ORDER (sequential k, Q after
-  every multiply and add) is the oracle's definition -- "parity unpinned" by
-  any reference test.
+* quant_gemm (per-op-rounded, lpq_quant_gemm) vs the reference's OWN
+  composition (mul -> quantize_fused_at -> add -> quantize_fused_at per k,
+  tests/golden/golden_gemm_v1.npz, made by tests/golden/make_golden_gemm.py
+  through oracle/_ref) and vs the restated oracle lpqo_quant_gemm (itself
+  pinned to that composition on the CPU, test_oracle_golden.py): bit-exact,
+  both kernels (hardware-bf16 fast path and the general path), every rounding
+  mode, and 64 sampled rows of the 4096^3 BASELINE problem.
 * quantized_matmul (lpq_matmul_q) vs the reference library's own
   quantized_matmul outputs (golden fixtures) and the oracle's double matmul.
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import pytest
 
@@ -109,19 +114,84 @@ def test_quant_gemm_identity_format_is_fp32_sequential(q):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
 
 
-def test_c4_quant_gemm_4096_sampled_rows(q, oracle):
+GOLDEN_GEMM = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                           "golden_gemm_v1.npz")
+
+
+def test_quant_gemm_vs_reference_composition_goldens(q):
+    """Every case the reference library produced through its own tensor ops
+    (bf16-exact inputs take k_qgemm_bf16, the rest k_qgemm_general), on the
+    device path and the host path."""
+    z = np.load(GOLDEN_GEMM)
+    n = 0
+    for ci, em, mm, ea, ma, mode, seed, call in z["meta"]:
+        a, b, want = z[f"a{ci}"], z[f"b{ci}"], z[f"c{ci}_{mode}"]
+        args = (q.FloatFormat(int(em), int(mm)), q.FloatFormat(int(ea), int(ma)),
+                q.RoundingMode(int(mode)), int(seed), int(call))
+        got = q.quant_gemm(dev(a), dev(b), *args).cpu().numpy()
+        assert np.array_equal(bits(got), bits(want)), (ci, mode)
+        got_h = q.quant_gemm(a, b, *args)
+        assert np.array_equal(bits(got_h), bits(want)), (ci, mode, "host")
+        n += 1
+    assert n == len(z["meta"]) >= 25
+
+
+def _sampled_rows(n, count=64, seed=0):
+    rng = np.random.default_rng(seed)
+    fixed = [0, 1, 127, 128, 255, 256, n // 2, n - 129, n - 128, n - 1]
+    extra = rng.choice(n, count - len(fixed), replace=False)
+    return sorted(set(fixed) | set(int(r) for r in extra))[:count]
+
+
+def _parallel_rows(fn, rows):
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+        return list(ex.map(fn, rows))
+
+
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
+def test_c4_quant_gemm_4096_sampled_rows(q, oracle, mode):
+    """C4 (4096^3, float(8,7) after every multiply and add): 64 sampled
+    output rows (tile borders included) vs the oracle, rows in parallel host
+    threads.  Nearest-even runs the bf16 path, stochastic the general path."""
     n = 4096
     a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
     b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
     f87 = q.QuantSpec(q.FloatFormat(8, 7))
     a = q.quantize_fused_at(a, f87, 0)
     b = q.quantize_fused_at(b, f87, 0)
-    c = q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7)).cpu().numpy()
+    c = q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7), q.RoundingMode(mode),
+                     0x15EED, 2).cpu().numpy()
     ah, bh = a.cpu().numpy(), b.cpu().numpy()
-    for r in (0, 1, 1777, 4095):
+    rows = _sampled_rows(n, 64, seed=mode)
+
+    def one(r):
         st, want = oracle.quant_gemm(ah[r:r + 1], bh, float_fmt(8, 7), float_fmt(8, 7),
-                                     row_base=r)
-        assert np.array_equal(bits(c[r:r + 1]), bits(want)), r
+                                     mode, seed=0x15EED, call=2, row_base=r)
+        return r, st == 0 and np.array_equal(bits(c[r:r + 1]), bits(want))
+    bad = [r for r, ok in _parallel_rows(one, rows) if not ok]
+    assert len(rows) == 64 and not bad, bad
+
+
+def test_matmul_q_4096_sampled_rows(q, oracle):
+    """The reference quantized_matmul at bench size (bench.py --config c4ref:
+    4096^3, fixed(8,4) stochastic, FP64 tensor-core DMMA + fused Q): 64
+    sampled rows vs the oracle's double matmul (tensor.cpp:355-376) and
+    quantizer with the rows' global index base."""
+    n = 4096
+    a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
+    b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
+    spec = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.Stochastic, 0x15EED)
+    c = q.quantized_matmul_at(a, b, spec, 0).cpu().numpy()
+    ah, bh = a.cpu().numpy(), b.cpu().numpy()
+    rows = _sampled_rows(n, 64, seed=7)
+
+    def one(r):
+        acc = oracle.matmul(ah[r:r + 1], bh)
+        st, want = oracle.quantize(acc, fixed_fmt(8, 4), STOCHASTIC, seed=0x15EED, call=0,
+                                   index_base=r * n)
+        return r, st == 0 and np.array_equal(bits(c[r:r + 1]), bits(want))
+    bad = [r for r, ok in _parallel_rows(one, rows) if not ok]
+    assert not bad, bad
 
 
 def test_matmul_q_vs_reference_goldens(q, oracle):

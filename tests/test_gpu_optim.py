@@ -5,7 +5,7 @@ oracle's quantizer and numpy fp32 ops (IEEE RN, == float(double op double)).
 import numpy as np
 import pytest
 
-from oracle_lib import STOCHASTIC, bits, fixed_fmt, float_fmt
+from oracle_lib import STOCHASTIC, bits, block_fmt, fixed_fmt, float_fmt
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -15,6 +15,8 @@ def oracle_fmt(f):
     import paper_1910_04540_b200 as q
     if isinstance(f, q.FloatFormat):
         return float_fmt(f.exp_bits, f.man_bits)
+    if isinstance(f, q.BlockFloatFormat):
+        return block_fmt(f.wl, f.block_dim)
     return fixed_fmt(f.wl, f.fl, f.symmetric, f.saturate)
 
 
@@ -54,7 +56,8 @@ class RefOpt:
         return out
 
 
-@pytest.mark.parametrize("cfg", ["wage_like", "float_all_stoch", "no_quant", "nearest_away"])
+@pytest.mark.parametrize("cfg", ["wage_like", "float_all_stoch", "no_quant", "nearest_away",
+                                 "block_all", "block_mixed"])
 def test_sgd_step_matches_reference_semantics(oracle, cfg):
     run_cfg(oracle, cfg, [(64, 33), (33,), (10, 64), (10,)])
 
@@ -80,6 +83,14 @@ def run_cfg(oracle, cfg, shapes, steps=4):
                                 accumulator=q.QuantSpec(q.FloatFormat(8, 7), S, 2, 5),
                                 gradient=q.QuantSpec(q.FloatFormat(4, 3), S, 3)),
         "no_quant": dict(),
+        # block floating point (the paper's training formats): the unfused
+        # per-parameter sequence (train.cpp:161-174) on the device
+        "block_all": dict(weight=q.QuantSpec(q.BlockFloatFormat(8, 0), E),
+                          accumulator=q.QuantSpec(q.BlockFloatFormat(16), S, 21),
+                          gradient=q.QuantSpec(q.BlockFloatFormat(8), S, 22)),
+        "block_mixed": dict(weight=q.QuantSpec(q.FixedFormat(8, 6), E),
+                            accumulator=q.QuantSpec(q.FloatFormat(8, 7), S, 2),
+                            gradient=q.QuantSpec(q.BlockFloatFormat(8, 0), S, 23)),
         "nearest_away": dict(weight=q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode.NearestAway),
                              gradient=q.QuantSpec(q.FixedFormat(6, 4, True, False),
                                                   q.RoundingMode.NearestTowardZero)),
@@ -105,7 +116,7 @@ def run_cfg(oracle, cfg, shapes, steps=4):
             assert spec.call_counter == ref.calls[k]
 
 
-def test_sgd_step_rejects_block_and_bad_args():
+def test_sgd_step_bad_args():
     import paper_1910_04540_b200 as q
     from paper_1910_04540_b200.optim import LowPrecisionOptimizer
     p = [torch.zeros(8, device="cuda")]
@@ -113,12 +124,23 @@ def test_sgd_step_rejects_block_and_bad_args():
         LowPrecisionOptimizer(p, lr=-1.0, momentum=0.5)
     with pytest.raises(q.FormatError):
         LowPrecisionOptimizer(p, lr=0.1, momentum=1.0)
-    opt = LowPrecisionOptimizer(p, lr=0.1, momentum=0.5,
-                                weight=q.QuantSpec(q.BlockFloatFormat(8)))
-    with pytest.raises(q.UnsupportedFormatError):
-        opt.step([torch.ones(8, device="cuda")])
     with pytest.raises(q.ShapeError):
         LowPrecisionOptimizer(p, 0.1, 0.5).step([torch.ones(9, device="cuda")])
+    # dtype / device: the kernel reads every pointer as n fp32 device values
+    with pytest.raises(TypeError):
+        LowPrecisionOptimizer([torch.zeros(8, device="cuda", dtype=torch.float16)], 0.1, 0.5)
+    with pytest.raises(TypeError):
+        LowPrecisionOptimizer([torch.zeros(8)], 0.1, 0.5)
+    opt = LowPrecisionOptimizer(p, 0.1, 0.5)
+    for g in (torch.ones(8, device="cuda", dtype=torch.bfloat16), torch.ones(8)):
+        with pytest.raises(TypeError):
+            opt.step([g])
+    # a rejected launch leaves the call counters untouched
+    bad = q.QuantSpec(q.FixedFormat(30, 4), q.RoundingMode.Stochastic, 1, 5)
+    opt = LowPrecisionOptimizer(p, 0.1, 0.5, gradient=bad)
+    with pytest.raises(q.FormatError):
+        opt.step([torch.ones(8, device="cuda")])
+    assert opt.grad_spec.call_counter == 5
 
 
 def test_sgd_step_async_equals_sync_and_defers_errors():

@@ -155,6 +155,9 @@ BLOCK_CASES = [
     ((6, 5, 9), 2),
     ((1, 3, 256), 1),       # leading 1: rows plan along dim 1
     ((257, 3), 0),          # stride 3 (< 64): columns plan along dim 0
+    ((70_001, 8), 1),       # narrow columns plan: 2 threads per row lane, 128 lanes
+    ((30_001, 6), 1),       # narrow, W % 4 != 0 (scalar loads), ragged lanes
+    ((9_000, 3, 20), 1),    # narrow, stride 20 inside a 60-float row
 ]
 
 
@@ -180,6 +183,31 @@ def test_block_plans_vs_oracle(q, oracle, shape, dim, mode, wl):
     # host path (streamed rows / resident two-pass)
     got_h = q.quantize_fused_at(x, spec_of(q, fmt, mode, seed=77), 3)
     assert same_bits(got_h, want)
+
+
+def test_block_columns_grid_y_beyond_65535(q, oracle):
+    """[2^20 + 3000, 1024] per column (block_dim=1, stride 1): the column
+    plans need more than 65535 row chunks, so grid.y is capped and the kernels
+    take the rest grid-stride (this used to fail the launch).
+    Sampled rows vs the oracle with the device-reduced block maxima, plus the
+    maxima themselves vs torch."""
+    R, W = (1 << 20) + 3000, 1024
+    x = q.random_uniform((R, W), 5, 0, -1.0, 1.0)
+    x[R - 1] = torch.linspace(-3.0, 3.0, W, device="cuda")   # max in the last chunk
+    for mode in (NEAREST_EVEN, STOCHASTIC):
+        fmt = block_fmt(8, 1)
+        spec = spec_of(q, fmt, mode, seed=9)
+        y = q.quantize_fused_at(x, spec, 4)
+        mx = x.abs().amax(dim=0)
+        dmx = q.block_absmax(x, spec.format).view(torch.float32)
+        assert torch.equal(dmx, mx)
+        mxh = mx.cpu().numpy()
+        for r in (0, 1, 16 * 65535 - 1, 16 * 65535, 16 * 65535 + 17, R - 2, R - 1):
+            xr = x[r:r + 1].cpu().numpy()
+            st, want = oracle.quantize_block_given_max(xr, fmt, mode, mxh, seed=9, call=4,
+                                                       index_base=r * W)
+            assert st == 0 and same_bits(y[r:r + 1], want), (mode, r)
+    del x, y
 
 
 def test_block_tiny_and_huge_maxima(q, oracle):
@@ -665,3 +693,33 @@ def test_host_path_byte_codes(q, fmt_name, mode):
     xp = torch.from_numpy(x).pin_memory()
     got_p = q.quantize_fused_at(xp, spec, 4)
     assert same_bits(got_p.numpy(), want), (fmt_name, mode)
+
+
+@pytest.mark.parametrize("case", ["fixed84", "float52", "block_whole", "block_dim1",
+                                  "block_tiny", "block_wl4_cols", "block_rows"])
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
+def test_direct_host_path_byte_codes(q, case, mode):
+    """Tensors <= 16 MB take the direct host path; formats whose every value
+    has a one-byte code copy codes device->host (fixed / float: ByteCode;
+    block wl <= 8 on the two-pass plans: k plus the block maxima), decoded on
+    the host.  Must equal the device path bit for bit, including blocks whose
+    results fall in the fp32 subnormal range (the encoder flags them and the
+    fp32 values are copied instead) and single-pass block plans (fp32)."""
+    fmt, shape, scale = {
+        "fixed84": (q.FixedFormat(8, 4), (1 << 20,), 8.0),
+        "float52": (q.FloatFormat(5, 2), (16384, 64), 1e3),
+        "block_whole": (q.BlockFloatFormat(8), (16384, 64), 4.0),   # criterion 7
+        "block_dim1": (q.BlockFloatFormat(8, 1), (4096, 256), 1.0),
+        "block_tiny": (q.BlockFloatFormat(8), (1 << 18,), 2.0 ** -140),
+        "block_wl4_cols": (q.BlockFloatFormat(4, 1), (333, 77), 1.0),
+        "block_rows": (q.BlockFloatFormat(8, 0), (512, 4096), 1.0),
+    }[case]
+    rng = np.random.default_rng(hash((case, mode)) % 2**32)
+    x = (rng.uniform(-1, 1, shape) * scale).astype(np.float32)
+    x.reshape(-1)[:4] = [0.0, -0.0, 1e-3 * scale, -1e-3 * scale]
+    spec = q.QuantSpec(fmt, q.RoundingMode(mode), 21)
+    want = q.quantize_fused_at(dev(x), spec, 2).cpu().numpy()
+    for host in (x, torch.from_numpy(x.copy()).pin_memory()):
+        got = q.quantize_fused_at(host, spec, 2)
+        got = got.numpy() if isinstance(got, torch.Tensor) else got
+        assert same_bits(got, want), (case, mode)

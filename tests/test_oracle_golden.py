@@ -136,3 +136,61 @@ def test_oracle_matches_reference_fixtures(oracle):
     v = np.array([oracle.variate(0x15EED, 0, i) for i in range(1000)], np.float32)
     assert np.array_equal(v, z["variates_15eed"])
     assert np.array_equal(oracle.matmul(z["mm_a"], z["mm_b"]), z["mm_c"])
+
+
+# ---- the per-op GEMM's rounding order, pinned to the reference itself ----------
+def _gemm_inputs(seed, m, k, n, scale_a=1.0, scale_b=1.0):
+    rng = np.random.default_rng(seed)
+    a = (rng.uniform(-1, 1, (m, k)) * scale_a).astype(np.float32)
+    b = (rng.uniform(-1, 1, (k, n)) * scale_b).astype(np.float32)
+    # edge values: zeros, exact powers of two, products on rounding ties,
+    # magnitudes that underflow / saturate the narrow formats
+    a.flat[::7] = 0.0
+    b.flat[3::11] = np.float32(-0.0)
+    a.flat[1::13] = np.float32(2.0 ** -9)
+    b.flat[2::17] = np.float32(1.5)
+    a.flat[5::19] = np.float32(3.0e4)
+    b.flat[4::23] = np.float32(-1.0e-6)
+    return a, b
+
+
+GEMM_CASES = [  # (fmt_mul, fmt_add, m, k, n, scale_a, scale_b)
+    ((8, 7), (8, 7), 6, 40, 5, 1.0, 1.0),
+    ((5, 2), (5, 2), 5, 33, 7, 1.0, 1.0),
+    ((4, 3), (4, 3), 4, 29, 6, 4.0, 0.25),
+    ((5, 2), (8, 7), 3, 64, 4, 16.0, 16.0),     # saturating products, wider adds
+    ((8, 23), (5, 10), 4, 17, 3, 1.0, 1.0),     # identity multiply, fp16-like adds
+    ((2, 1), (3, 0), 3, 12, 3, 1.0, 1.0),       # tiny formats (max 6, 2-point grids)
+]
+
+
+@pytest.mark.parametrize("case", GEMM_CASES, ids=str)
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, NEAREST_AWAY, NEAREST_ZERO, STOCHASTIC])
+def test_quant_gemm_restatement_equals_reference_composition(oracle, ref, case, mode):
+    """The restated per-op GEMM (oracle/lpq_oracle.c lpqo_quant_gemm, which
+    the device kernels are checked against) equals, bit for bit, the
+    reference's OWN composition per k: mul -> quantize_fused_at(call+2k) ->
+    add -> quantize_fused_at(call+2k+1) (tensor.cpp:140-156,
+    quant_ops.cpp:154-164) -- so the rounding order and the
+    stochastic call mapping are pinned to the reference library."""
+    (em, mm), (ea, ma), m, k, n, sa, sb = case
+    a, b = _gemm_inputs(hash((case, mode)) % 2**32, m, k, n, sa, sb)
+    fm, fa = float_fmt(em, mm), float_fmt(ea, ma)
+    st, want = ref.quant_gemm_composed(a, b, fm, fa, mode, seed=0x15EED, call=9)
+    assert st == 0
+    st, got = oracle.quant_gemm(a, b, fm, fa, mode, seed=0x15EED, call=9)
+    assert st == 0
+    assert np.array_equal(bits(got), bits(want)), (case, mode)
+
+
+def test_oracle_quant_gemm_matches_reference_gemm_fixtures(oracle):
+    """The restated per-op GEMM vs every fixture the reference produced
+    through its own tensor-op composition (tests/golden/golden_gemm_v1.npz)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "golden_gemm_v1.npz"))
+    for ci, em, mm, ea, ma, mode, seed, call in z["meta"]:
+        st, got = oracle.quant_gemm(z[f"a{ci}"], z[f"b{ci}"], float_fmt(int(em), int(mm)),
+                                    float_fmt(int(ea), int(ma)), int(mode), seed=int(seed),
+                                    call=int(call))
+        assert st == 0 and np.array_equal(bits(got), bits(z[f"c{ci}_{mode}"])), (ci, mode)
