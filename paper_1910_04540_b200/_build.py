@@ -35,7 +35,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 SOURCES = ["capi.cu", "runtime.cu", "elementwise.cu", "block.cu",
-           "block_cluster.cu", "gemm.cu", "composed.cu", "optim.cu",
+           "block_cluster.cu", "block_chunks.cu", "gemm.cu", "composed.cu", "optim.cu",
            "group.cu", "io.cu"]
 HEADERS = ["quant_math.cuh", "kernels.cuh", "runtime.h", "block_common.cuh"]
 

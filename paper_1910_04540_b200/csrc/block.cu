@@ -523,6 +523,8 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
     launch_rows<M>(x, y, g.stride, g.extent, base, key, wl, status, s);
     return cudaGetLastError();
   }
+  if (plan == BlockPlan::kRowsChunked)
+    return launch_block_chunks(x, y, g.stride, g.extent, base, key, wl, M, ws, status, s);
   if (plan == BlockPlan::kRowsCluster)
     return launch_block_cluster(x, y, g.stride, g.extent, base, key, wl, M,
                                 status, s);
@@ -634,6 +636,10 @@ bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y) {
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
   const bool rows = g.outer == 1 && g.stride % 4 == 0 && aligned16(x) && aligned16(y);
   if (rows && g.stride <= 32768 && g.stride >= 4) return BlockPlan::kRowsInRegisters;
+  // longer rows of up to ~1M floats: chunk rendezvous (one HBM pass, every
+  // SM busy; needs the workspace -- quantize_device takes the cluster plan
+  // when the caller supplied none)
+  if (rows && block_chunks_ok(g.stride, g.extent)) return BlockPlan::kRowsChunked;
   // cluster plan: rows of at most 1M floats (L2-resident second read) and
   // enough (row, CTA) pairs to fill the SMs; a few huge rows stream through
   // every SM with the two-pass segment plan instead (quantize_device still
@@ -646,6 +652,7 @@ BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
 }
 
 size_t block_workspace(const BlockGeom& g, BlockPlan p) {
+  if (p == BlockPlan::kRowsChunked) return block_chunks_workspace(g.extent);
   if (block_plan_single_pass(p)) return 0;
   return (size_t)(((g.extent * 4) + 255) / 256 * 256);
 }

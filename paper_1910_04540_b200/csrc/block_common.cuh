@@ -70,12 +70,8 @@ __device__ __forceinline__ bool needs_guard(const BlockScale& s) {
 }
 
 // |x| maximum that PROPAGATES NaN (FMNMX3.NAN, 0.5 instructions per
-// element); a NaN row maximum sends the row down absmax_nf's slow path.
-__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
-  float d;
-  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
+// element, fmax3_nan in quant_math.cuh); a NaN row maximum sends the row
+// down absmax_nf's slow path.
 __device__ __forceinline__ void absmax_nan(const float4& v, float& m) {
   m = fmax3_nan(m, fabsf(v.x), fabsf(v.y));
   m = fmax3_nan(m, fabsf(v.z), fabsf(v.w));

@@ -11,6 +11,7 @@
 // LPQ_ERR_CUDA with the message kept in lpq_last_cuda_error().
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <mutex>
@@ -33,7 +34,14 @@ std::vector<bool> g_dev_known;
 }  // namespace
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
-void note_passes(int n) { g_passes.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+namespace {
+thread_local int t_pass_scope = 0;  // > 0: inside a host call that counts itself
+}
+void note_passes(int n) {
+  if (t_pass_scope == 0) g_passes.fetch_add((uint64_t)n, std::memory_order_relaxed);
+}
+PassScope::PassScope() { ++t_pass_scope; }
+PassScope::~PassScope() { --t_pass_scope; }
 
 lpq_status cuda_fail(cudaError_t e) {
   t_cuda_error = cudaGetErrorString(e);
@@ -200,7 +208,8 @@ size_t lpq_workspace_size(const lpq_format* f, const int64_t* shape, int rank) {
   BlockGeom g;
   if (block_geometry(f, shape, rank, &g) != LPQ_OK) return 0;
   // upper bound over plans (the plan also depends on pointer alignment)
-  return block_workspace(g, BlockPlan::kTwoPassColumns);
+  return std::max(block_workspace(g, BlockPlan::kTwoPassColumns),
+                  block_workspace(g, BlockPlan::kRowsChunked));
 }
 
 uint64_t lpq_launch_count(void) { return g_launches.load(); }

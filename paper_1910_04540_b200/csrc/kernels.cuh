@@ -40,15 +40,20 @@ struct BlockGeom {
 };
 
 // Which plan a block quantization uses (and how many HBM passes it makes).
-enum class BlockPlan { kRowsInRegisters, kRowsCluster, kTwoPassSegments,
-                       kTwoPassColumns };
+enum class BlockPlan { kRowsInRegisters, kRowsCluster, kRowsChunked,
+                       kTwoPassSegments, kTwoPassColumns };
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y);
 // the cluster (single-pass) plan can run this geometry
 bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y);
 inline int block_plan_passes(BlockPlan p) {
-  return (p == BlockPlan::kRowsInRegisters || p == BlockPlan::kRowsCluster) ? 1 : 2;
+  return (p == BlockPlan::kRowsInRegisters || p == BlockPlan::kRowsCluster ||
+          p == BlockPlan::kRowsChunked) ? 1 : 2;
 }
 inline bool block_plan_single_pass(BlockPlan p) { return block_plan_passes(p) == 1; }
+// the plan leaves max|x| bits per block in ws[0 .. extent) (u32)
+inline bool block_plan_maxima_in_ws(BlockPlan p) {
+  return p == BlockPlan::kRowsChunked || !block_plan_single_pass(p);
+}
 // cluster plan (block_cluster.cu): CTAs per row for a contiguous block of L
 // floats, 0 if too long
 int cluster_size_for(int64_t L);
@@ -56,7 +61,16 @@ cudaError_t launch_block_cluster(const float* x, float* y, int64_t L,
                                  int64_t nrows, uint64_t base, uint64_t key,
                                  int wl, int mode, uint32_t* status,
                                  cudaStream_t s);
-// Workspace bytes for a plan: extent uint32 maxima (two-pass plans only).
+// chunk-rendezvous plan (block_chunks.cu): nrows contiguous rows of L floats
+// (L % 4 == 0, 16-byte aligned x / y), single HBM pass, workspace
+// block_chunks_workspace(nrows) bytes (rowmax[nrows] first)
+bool block_chunks_ok(int64_t L, int64_t nrows);
+size_t block_chunks_workspace(int64_t nrows);
+cudaError_t launch_block_chunks(const float* x, float* y, int64_t L, int64_t nrows,
+                                uint64_t base, uint64_t key, int wl, int mode, void* ws,
+                                uint32_t* status, cudaStream_t s);
+// Workspace bytes for a plan: extent uint32 maxima (two-pass plans), the
+// chunk plan's row state; 0 for the other single-pass plans.
 size_t block_workspace(const BlockGeom& g, BlockPlan p);
 
 cudaError_t launch_block(const float* x, float* y, const BlockGeom& g,

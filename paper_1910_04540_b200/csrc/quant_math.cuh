@@ -295,6 +295,73 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
   }
 }
 
+// 3-input maximum that propagates NaN / 3-input minimum (NaN operands
+// ignored): one FMNMX3 each
+LPQ_HD float fmax3_nan(float a, float b, float c) {
+#if defined(__CUDA_ARCH__)
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+#else
+  if (a != a || b != b || c != c) return a + b + c;
+  return fmaxf(fmaxf(a, b), c);
+#endif
+}
+LPQ_HD float fmin3(float a, float b, float c) {
+#if defined(__CUDA_ARCH__)
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+#else
+  return fminf(fminf(a, b), c);
+#endif
+}
+
+// mad.lo.u32 against a runtime multiplier (RngMul::one): an add that issues
+// on the FMA pipe as an IMAD instead of an ALU IADD3
+LPQ_HD uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+#else
+  return a * b + c;
+#endif
+}
+
+// variate24_x4 for the ALU-pipe-bound float kernels, returning the TOP
+// words of the last product (variate = top >> 8; the low 8 bits are hash
+// bits the caller ignores): the lane add as an IMAD against m.one and the
+// >> 27 xor-shift as IMAD.HI / IMAD against m.m32 (as variate24_zb), so
+// more of the hash issues on the FMA pipe; quant_float_bits_top folds the
+// >> 8 into its own shift.  Identical variates to variate24_z.
+LPQ_HD void variate24_x4_top(uint64_t key, uint64_t idx, const RngMul& m,
+                             uint32_t out[4]) {
+  const uint64_t z0 = key ^ idx;
+  const uint64_t w = (z0 & ~3ull) + 0x9E3779B97F4A7C15ull;
+  const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
+  const uint32_t kl = (uint32_t)key & 3u;
+  if (wlo > 0xFFFFFFFCu) {  // w + j_q may carry into the high word
+    for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m.m32) << 8;
+    return;
+  }
+  const uint32_t h1 = whi ^ (whi >> 30);                   // shared
+  const uint64_t hc = (uint64_t)(h1 * 0x1CE4E5B9u) << 32;  // shared hi*C1lo
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t lo = mad_lo(kl ^ (uint32_t)q, m.one, wlo);
+    lo ^= funnel_r<30>(lo, whi);
+    const uint64_t p = (uint64_t)lo * 0x1CE4E5B9u + hc;    // z *= C1
+    uint32_t plo = (uint32_t)p;
+    uint32_t phi = (uint32_t)(p >> 32) + lo * 0xBF58476Du;
+    const uint32_t slo = umulhi32(plo, m.m32) + phi * m.m32;  // (z >> 27).lo
+    const uint32_t shi = umulhi32(phi, m.m32);                // (z >> 27).hi
+    plo ^= slo;
+    phi ^= shi;
+    out[q] = mulhi_sep(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
+  }
+}
+
 // ---- magnitude rounding ---------------------------------------------------
 //
 // a = |r| where r = x * 2^s was formed in fp32; a is exact unless it fell
@@ -479,6 +546,7 @@ struct FloatParams {
   uint32_t rodd;     // 1; 0 for man == 0, where k = 1 is always odd (rhalf
                      // then carries the +1: ties round up to k = 2)
   uint32_t vshift;   // 1 + man (stochastic: R = (~v & 0xFFFFFF) >> vshift)
+  uint32_t vshift8;  // vshift + 8 (quant_float_bits_top: v = top >> 8)
   float min_normal;  // 2^min_exp
   uint32_t m_neg23;  // -2^23 (mod 2^32)
   uint32_t m_pos23;  // 2^23
@@ -519,6 +587,7 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.rodd = man_bits == 0 ? 0u : 1u;
   p.rshift = man_bits <= 22 ? (uint32_t)(23 - man_bits) : 0u;
   p.vshift = (uint32_t)(1 + man_bits);
+  p.vshift8 = p.vshift + 8u;
   p.min_normal = p.min_exp >= -126 ? u2f((uint32_t)(127 + p.min_exp) << 23) : 0.0f;
   return p;
 }
@@ -630,6 +699,24 @@ LPQ_HD float quant_float_bits(float xc, const FloatParams& p, uint32_t v) {
   } else {
     b += p.rhalf + ((b >> p.rshift) & p.rodd);
   }
+  return u2f(b & ~p.rmask);
+}
+
+// quant_float_bits<kStochastic> from the variate's top word (v = top >> 8,
+// the low 8 bits of top arbitrary): the sign spread as IMAD.HI.S32 and the
+// carry add as IMAD against the runtime one (FMA pipe), and
+// (top ^ (~neg & 0xFFFFFF00)) >> (8 + vshift) == (v ^ (~neg & 0xFFFFFF)) >> vshift.
+LPQ_HD float quant_float_bits_top(float xc, const FloatParams& p, uint32_t top,
+                                  uint32_t one) {
+  uint32_t b = f2u(xc);
+#if defined(__CUDA_ARCH__)
+  int32_t neg;  // all ones iff x < 0: the high word of b * 1, signed
+  asm("mul.hi.s32 %0, %1, %2;" : "=r"(neg) : "r"((int32_t)b), "r"((int32_t)one));
+#else
+  const int32_t neg = (int32_t)b >> 31;
+#endif
+  const uint32_t r = (top ^ (~(uint32_t)neg & 0xFFFFFF00u)) >> p.vshift8;
+  b = mad_lo(r, one, b);
   return u2f(b & ~p.rmask);
 }
 

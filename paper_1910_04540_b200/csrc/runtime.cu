@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -42,6 +44,8 @@ struct HostCtx {
   float* pin_out[kStreams] = {};
   uint8_t* dcode[kStreams] = {};   // device byte codes of a chunk
   uint8_t* pcode[kStreams] = {};   // page-locked byte codes of a chunk
+  void* sws[kStreams] = {};        // device workspace of a chunk's call
+  size_t sws_bytes = 0;
   int64_t chunk_cap = 0;  // elements per chunk buffer
   uint32_t* d_status = nullptr;
   void* ws = nullptr;
@@ -58,6 +62,11 @@ struct HostCtx {
   uint32_t* daux = nullptr;  // device: encode flag
   uint32_t* paux = nullptr;  // page-locked: block maxima [extent] + flag
   int64_t paux_cap = 0;
+  // direct pipeline: per part, "copied in" and "codes back" events
+  static constexpr int kParts = 8;
+  cudaEvent_t ev_in[kParts] = {};
+  cudaEvent_t ev_out[kParts] = {};
+  uint32_t* pstatus = nullptr;  // page-locked status word (status fetch)
   std::mutex mu;
 
   ~HostCtx() { release(); }
@@ -70,8 +79,10 @@ struct HostCtx {
       if (pin_out[k]) cudaFreeHost(pin_out[k]);
       if (dcode[k]) cudaFree(dcode[k]);
       if (pcode[k]) cudaFreeHost(pcode[k]);
+      if (sws[k]) cudaFree(sws[k]);
       dcode[k] = nullptr;
       pcode[k] = nullptr;
+      sws[k] = nullptr;
       if (done[k]) cudaEventDestroy(done[k]);
       if (st[k]) cudaStreamDestroy(st[k]);
       dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
@@ -86,6 +97,13 @@ struct HostCtx {
     if (pcodef) cudaFreeHost(pcodef);
     if (daux) cudaFree(daux);
     if (paux) cudaFreeHost(paux);
+    if (pstatus) cudaFreeHost(pstatus);
+    pstatus = nullptr;
+    for (int k = 0; k < kParts; ++k) {
+      if (ev_in[k]) cudaEventDestroy(ev_in[k]);
+      if (ev_out[k]) cudaEventDestroy(ev_out[k]);
+      ev_in[k] = ev_out[k] = nullptr;
+    }
     pstage = nullptr;
     dcodef = nullptr;
     pcodef = nullptr;
@@ -95,7 +113,7 @@ struct HostCtx {
     ws = nullptr;
     dfull = nullptr;
     chunk_cap = dfull_cap = 0;
-    ws_bytes = 0;
+    ws_bytes = sws_bytes = 0;
   }
 
   cudaError_t init() {
@@ -106,9 +124,28 @@ struct HostCtx {
       e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
       if (e != cudaSuccess) return e;
     }
-    cudaError_t e = cudaMalloc(&d_status, sizeof(uint32_t));
+    for (int k = 0; k < kParts; ++k) {
+      cudaError_t e = cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaMallocHost(&pstatus, sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&d_status, sizeof(uint32_t));
     if (e != cudaSuccess) return e;
     return cudaMemset(d_status, 0, sizeof(uint32_t));
+  }
+
+  // lpq_status_fetch through the page-locked status word (a pageable
+  // 4-byte copy costs tens of microseconds)
+  lpq_status fetch_status(cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(pstatus, d_status, sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    const uint32_t bits = *pstatus;
+    if (e == cudaSuccess && bits) e = cudaMemsetAsync(d_status, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return map_status_bits(bits);
   }
 
   cudaError_t ensure_chunks(int64_t elems) {
@@ -119,20 +156,27 @@ struct HostCtx {
       if (pin_out[k]) cudaFreeHost(pin_out[k]);
       if (dcode[k]) cudaFree(dcode[k]);
       if (pcode[k]) cudaFreeHost(pcode[k]);
+      if (sws[k]) cudaFree(sws[k]);
       dbuf[k] = pin_in[k] = pin_out[k] = nullptr;
       dcode[k] = pcode[k] = nullptr;
+      sws[k] = nullptr;
     }
     chunk_cap = 0;
+    sws_bytes = 0;
     const size_t bytes = sizeof(float) * (size_t)elems;
+    // a chunk's block call: the row plans' state for rows > 32768 floats
+    const size_t wsb = block_chunks_workspace(elems / 32768 + 1);
     for (int k = 0; k < kStreams; ++k) {
       cudaError_t e = cudaMalloc(&dbuf[k], bytes);
       if (e == cudaSuccess) e = cudaMallocHost(&pin_in[k], bytes);
       if (e == cudaSuccess) e = cudaMallocHost(&pin_out[k], bytes);
       if (e == cudaSuccess) e = cudaMalloc(&dcode[k], (size_t)elems);
       if (e == cudaSuccess) e = cudaMallocHost(&pcode[k], (size_t)elems);
+      if (e == cudaSuccess) e = cudaMalloc(&sws[k], wsb);
       if (e != cudaSuccess) return e;
     }
     chunk_cap = elems;
+    sws_bytes = wsb;
     return cudaSuccess;
   }
 
@@ -256,7 +300,9 @@ class CopyPool {
     }
     next_ = 0;
     pending_ = jobs_.size();
+    apending_.store(pending_, std::memory_order_release);
     ++gen_;
+    agen_.store(gen_, std::memory_order_release);
     lk.unlock();
     cv_.notify_all();
     exec(Job{dst, src, std::min(part, count), dec, first});
@@ -268,6 +314,12 @@ class CopyPool {
       exec(j);
       lk.lock();
       --pending_;
+      apending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+    if (pending_ != 0) {  // spin briefly (the parts finish within microseconds)
+      lk.unlock();
+      spin_until([&] { return apending_.load(std::memory_order_acquire) == 0; });
+      lk.lock();
     }
     done_.wait(lk, [&] { return pending_ == 0; });
   }
@@ -317,10 +369,28 @@ class CopyPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
+  // poll pred for up to ~200 us before the caller falls back to blocking:
+  // a host call issues its pool jobs back to back, and a condition-variable
+  // wake-up costs tens of microseconds on this host
+  template <class P>
+  static bool spin_until(P pred) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0;; ++i) {
+      if (pred()) return true;
+      if ((i & 63) == 63 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200))
+        return false;
+    }
+  }
   void loop() {
     uint64_t seen = 0;
     std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
+      if (!stop_ && !(gen_ != seen && next_ < jobs_.size())) {
+        lk.unlock();
+        spin_until([&] { return agen_.load(std::memory_order_acquire) != seen; });
+        lk.lock();
+      }
       cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < jobs_.size()); });
       if (stop_) return;
       while (next_ < jobs_.size()) {
@@ -328,6 +398,7 @@ class CopyPool {
         lk.unlock();
         exec(j);
         lk.lock();
+        apending_.fetch_sub(1, std::memory_order_acq_rel);
         if (--pending_ == 0) done_.notify_all();
       }
       seen = gen_;
@@ -339,6 +410,8 @@ class CopyPool {
   std::vector<Job> jobs_;
   size_t next_ = 0, pending_ = 0;
   uint64_t gen_ = 0;
+  std::atomic<uint64_t> agen_{0};      // gen_, for the spinning workers
+  std::atomic<size_t> apending_{0};    // pending_, for the spinning caller
   bool stop_ = false;
 };
 
@@ -346,8 +419,10 @@ std::mutex g_copy_mu;  // one parallel copy at a time (the pool is shared)
 
 void parallel_memcpy(void* dst, const void* src, size_t bytes,
                      size_t serial_below = size_t(8) << 20) {
-  // below serial_below the workers' wake-up costs more than the copy
-  const size_t kMinPart = size_t(1) << 20;
+  // below serial_below the workers' wake-up costs more than the copy; parts
+  // of >= 256 KB (4 MB: 16 threads 11 us, 4 threads 28 us, 1 thread 228 us,
+  // scripts/host_copy_probe.cpp)
+  const size_t kMinPart = size_t(256) << 10;
   const size_t want = bytes < serial_below ? 1 : bytes / kMinPart;
   if (want <= 1) {
     std::memcpy(dst, src, bytes);
@@ -367,7 +442,7 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes,
 // per part, like the copies); first: tensor index of codes[0]
 void parallel_decode(float* dst, const uint8_t* codes, size_t n, const Decode& dec,
                      size_t first = 0) {
-  const size_t kMinPart = size_t(1) << 18;
+  const size_t kMinPart = size_t(1) << 15;  // 32K codes (1M: 8 threads 14 us)
   const size_t want = std::max<size_t>(1, n / kMinPart);
   std::lock_guard<std::mutex> lk(g_copy_mu);
   CopyPool& pool = CopyPool::get();
@@ -497,7 +572,7 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
     else { shp[0] = len; rank = 1; }
     qst = quantize_device(c->dbuf[k], c->dbuf[k], shp, rank,
                           index_base + (uint64_t)off, &fr, mode, seed, call,
-                          nullptr, 0, c->d_status, c->st[k]);
+                          c->sws[k], c->sws_bytes, c->d_status, c->st[k]);
     if (qst != LPQ_OK) break;
     if (coded) {  // a quarter of the bytes across PCIe; decoded in finish()
       LPQ_TRY(launch_encode8(c->dbuf[k], c->dcode[k], len, bc, c->st[k]));
@@ -566,46 +641,50 @@ lpq_status resident_quantize(HostCtx* c, const float* x, float* y,
 }
 
 // Host -> device copy of a whole (small) tensor: pinned memory directly;
-// pageable memory staged through the context's page-locked buffer by the
-// copy pool (1 MB parts) -- the driver's own staging of pageable copies runs
-// at a fraction of PCIe (scripts/time_host.py).
+// pageable memory through the context's page-locked staging buffer, filled
+// by the copy pool (the driver's own staging of pageable copies runs at
+// ~18 GB/s on the B200 host, scripts/host_copy_probe.cpp: 232 us for 4 MB
+// against ~11 us of pool memcpy + 86 us of DMA).
 cudaError_t h2d_small(HostCtx* c, float* d, const float* x, int64_t n, cudaStream_t s) {
   const size_t bytes = sizeof(float) * (size_t)n;
-  if (is_pinned(x) || bytes < (size_t(1) << 20))
+  if (is_pinned(x) || bytes < (size_t(256) << 10))
     return cudaMemcpyAsync(d, x, bytes, cudaMemcpyHostToDevice, s);
   cudaError_t e = c->ensure_stage(n);
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(s);  // the staging buffer may still feed a copy
   if (e != cudaSuccess) return e;
-  parallel_memcpy(c->pstage, x, bytes, size_t(1) << 20);
+  parallel_memcpy(c->pstage, x, bytes, size_t(256) << 10);
   return cudaMemcpyAsync(d, c->pstage, bytes, cudaMemcpyHostToDevice, s);
 }
 
 // Device -> host copy of a whole (small) tensor, then the status fetch
-// (which synchronises the stream).
+// (which synchronises the stream); pageable destinations through the
+// staging buffer (DMA, then the copy pool).
 lpq_status d2h_small_and_fetch(HostCtx* c, float* y, const float* d, int64_t n,
                                cudaStream_t s) {
   const size_t bytes = sizeof(float) * (size_t)n;
-  if (is_pinned(y) || bytes < (size_t(1) << 20)) {
+  if (is_pinned(y) || bytes < (size_t(256) << 10)) {
     LPQ_TRY(cudaMemcpyAsync(y, d, bytes, cudaMemcpyDeviceToHost, s));
-    return lpq_status_fetch(c->d_status, s);
+    return c->fetch_status(s);
   }
   LPQ_TRY(c->ensure_stage(n));
   LPQ_TRY(cudaMemcpyAsync(c->pstage, d, bytes, cudaMemcpyDeviceToHost, s));
-  const lpq_status st = lpq_status_fetch(c->d_status, s);
+  const lpq_status st = c->fetch_status(s);
   if (st != LPQ_OK) return st;
-  parallel_memcpy(y, c->pstage, bytes, size_t(1) << 20);
+  parallel_memcpy(y, c->pstage, bytes, size_t(256) << 10);
   return LPQ_OK;
 }
 
-// Small tensors (<= 16 MB): one copy in, the device call, one copy out on
-// one stream.  Below ~16 MB the chunked pipeline's per-chunk events, waits
-// and bounce copies cost more than the overlap they buy (scripts/time_host.py).
-// Formats whose every quantized value has a one-byte code (ByteCode: fixed
-// wl <= 8 saturating, float 1 + exp + man <= 8; block wl <= 8 on the
-// two-pass plans, whose maxima give each block's step) copy the codes back
-// instead of fp32: a quarter of the device->host bytes, decoded bit-exactly
-// on the host.
+// Small tensors (<= 16 MB).  Formats whose every quantized value has a
+// one-byte code (ByteCode: fixed wl <= 8 saturating, float 1 + exp + man <=
+// 8) run as a pipeline of up to kParts parts over two streams: the input is
+// staged once (pool memcpy into page-locked memory), then part k's H2D copy
+// (stream 0) overlaps part k-1's kernels and code copy-back (stream 1, on
+// the other copy engine), and the host decodes part k-1 while part k is in
+// flight.  A quarter of the device->host bytes cross PCIe, decoded
+// bit-exactly on the host.  Block formats with wl <= 8 whose plan leaves the
+// block maxima in the workspace also copy codes back (decoded with each
+// block's step); everything else copies fp32.
 lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
                            const int64_t* shape, int rank, int64_t n,
                            uint64_t index_base, const lpq_format* f, int mode,
@@ -614,6 +693,61 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
   const size_t wsb = lpq_workspace_size(f, shape, rank);
   if (wsb) LPQ_TRY(c->ensure_ws(wsb));
   cudaStream_t s = c->st[0];
+  ByteCode bc{};
+  float lut[256];
+  const bool coded = byte_code_for(f, mode, &bc, lut);
+  if (coded && f->kind != LPQ_BLOCK) {
+    // validate once (the parts' device calls see 1-D pieces)
+    lpq_status st = check_format(f);
+    if (st != LPQ_OK) return st;
+    LPQ_TRY(c->ensure_codes(n, 1));
+    const int64_t parts = std::max<int64_t>(
+        1, std::min<int64_t>(HostCtx::kParts, n / (int64_t(1) << 17)));
+    const int64_t part = ((n + parts - 1) / parts + 1023) / 1024 * 1024;
+    const float* src = x;
+    if (!is_pinned(x)) {
+      LPQ_TRY(c->ensure_stage(n));
+      parallel_memcpy(c->pstage, x, sizeof(float) * (size_t)n, size_t(256) << 10);
+      src = c->pstage;
+    }
+    cudaStream_t s1 = c->st[1];
+    const Decode dec = decoder_for(f, bc, lut);
+    lpq_status qst = LPQ_OK;
+    int64_t issued = 0;
+    {
+      PassScope scope;  // one data pass for the whole call, counted below
+      for (int64_t k = 0, off = 0; off < n; ++k, off += part) {
+        const int64_t len = std::min(part, n - off);
+        LPQ_TRY(cudaMemcpyAsync(c->dfull + off, src + off, sizeof(float) * (size_t)len,
+                                cudaMemcpyHostToDevice, s));
+        LPQ_TRY(cudaEventRecord(c->ev_in[k], s));
+        LPQ_TRY(cudaStreamWaitEvent(s1, c->ev_in[k], 0));
+        const int64_t shp[1] = {len};
+        qst = quantize_device(c->dfull + off, c->dfull + off, shp, 1, index_base + (uint64_t)off,
+                              f, mode, seed, call, nullptr, 0, c->d_status, s1);
+        if (qst != LPQ_OK) break;
+        LPQ_TRY(launch_encode8(c->dfull + off, c->dcodef + off, len, bc, s1));
+        LPQ_TRY(cudaMemcpyAsync(c->pcodef + off, c->dcodef + off, (size_t)len,
+                                cudaMemcpyDeviceToHost, s1));
+        LPQ_TRY(cudaEventRecord(c->ev_out[k], s1));
+        ++issued;
+      }
+    }
+    note_passes(1);
+    if (qst != LPQ_OK) {
+      cudaStreamSynchronize(s);
+      cudaStreamSynchronize(s1);
+      return qst;
+    }
+    // decode part by part as the codes land (statuses are checked at the
+    // end: a flagged call discards its output, like the reference's throw)
+    for (int64_t k = 0; k < issued; ++k) {
+      const int64_t off = k * part, len = std::min(part, n - off);
+      LPQ_TRY(cudaEventSynchronize(c->ev_out[k]));
+      parallel_decode(y + off, c->pcodef + off, (size_t)len, dec);
+    }
+    return c->fetch_status(s1);
+  }
   LPQ_TRY(h2d_small(c, c->dfull, x, n, s));
   const lpq_status qst = quantize_device(c->dfull, c->dfull, shape, rank, index_base,
                                          f, mode, seed, call, c->ws, c->ws_bytes,
@@ -622,35 +756,24 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
     cudaStreamSynchronize(s);
     return qst;
   }
-  ByteCode bc{};
-  float lut[256];
-  const bool coded = byte_code_for(f, mode, &bc, lut);
   BlockGeom g{1, 1, n};
   bool bcoded = false;
   if (!coded && f->kind == LPQ_BLOCK && f->wl <= 8 &&
       (mode == kNearestEven || mode == kStochastic) &&
       block_geometry(f, shape, rank, &g) == LPQ_OK)
-    bcoded = !block_plan_single_pass(block_plan(g, c->dfull, c->dfull));
-  if (!coded && !bcoded) return d2h_small_and_fetch(c, y, c->dfull, n, s);
+    bcoded = block_plan_maxima_in_ws(block_plan(g, c->dfull, c->dfull));
+  if (!bcoded) return d2h_small_and_fetch(c, y, c->dfull, n, s);
   LPQ_TRY(c->ensure_codes(n, g.extent));
-  if (coded) {
-    LPQ_TRY(launch_encode8(c->dfull, c->dcodef, n, bc, s));
-  } else {
-    LPQ_TRY(cudaMemsetAsync(c->daux, 0, sizeof(uint32_t), s));
-    LPQ_TRY(launch_encode_block8(c->dfull, c->dcodef, g, static_cast<const uint32_t*>(c->ws),
-                                 f->wl, c->daux, s));
-    LPQ_TRY(cudaMemcpyAsync(c->paux, c->ws, sizeof(uint32_t) * (size_t)g.extent,
-                            cudaMemcpyDeviceToHost, s));
-    LPQ_TRY(cudaMemcpyAsync(c->paux + g.extent, c->daux, sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, s));
-  }
+  LPQ_TRY(cudaMemsetAsync(c->daux, 0, sizeof(uint32_t), s));
+  LPQ_TRY(launch_encode_block8(c->dfull, c->dcodef, g, static_cast<const uint32_t*>(c->ws),
+                               f->wl, c->daux, s));
+  LPQ_TRY(cudaMemcpyAsync(c->paux, c->ws, sizeof(uint32_t) * (size_t)g.extent,
+                          cudaMemcpyDeviceToHost, s));
+  LPQ_TRY(cudaMemcpyAsync(c->paux + g.extent, c->daux, sizeof(uint32_t),
+                          cudaMemcpyDeviceToHost, s));
   LPQ_TRY(cudaMemcpyAsync(c->pcodef, c->dcodef, (size_t)n, cudaMemcpyDeviceToHost, s));
-  const lpq_status st = lpq_status_fetch(c->d_status, s);
+  const lpq_status st = c->fetch_status(s);
   if (st != LPQ_OK) return st;
-  if (coded) {
-    parallel_decode(y, c->pcodef, (size_t)n, decoder_for(f, bc, lut));
-    return LPQ_OK;
-  }
   if (c->paux[g.extent] != 0u)  // a result in the subnormal range: fp32 copy
     return d2h_small_and_fetch(c, y, c->dfull, n, s);
   std::vector<double> delta((size_t)g.extent);

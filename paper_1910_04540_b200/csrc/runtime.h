@@ -10,6 +10,13 @@
 namespace lpq {
 
 void note_passes(int n);
+// While alive, the calling thread's device calls do not count data passes: a
+// host entry point that streams one tensor through several device calls
+// (chunks) counts the passes of the whole tensor once itself.
+struct PassScope {
+  PassScope();
+  ~PassScope();
+};
 lpq_status cuda_fail(cudaError_t e);
 lpq_status check_format(const lpq_format* f);
 lpq_status check_shape(const int64_t* shape, int rank, int64_t* numel);

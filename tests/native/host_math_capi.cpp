@@ -105,5 +105,31 @@ void hm_variates24_fma(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
 void hm_variates24_x4(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   for (int64_t i = 0; i < n; i += 4) lpq::variate24_x4(key, base + (uint64_t)i, 32u, out + i);
 }
+// the top-word float4 form (variate = top >> 8)
+void hm_variates24_x4_top(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  const lpq::RngMul m = lpq::rng_mul();
+  for (int64_t i = 0; i < n; i += 4) {
+    lpq::variate24_x4_top(key, base + (uint64_t)i, m, out + i);
+    for (int q = 0; q < 4; ++q) out[i + q] >>= 8;
+  }
+}
+// stochastic bit-domain float quantizer from top words (v << 8 | junk):
+// clamped inputs in the bit-domain range only (the caller filters)
+void hm_quant_float_bits_top(const float* x, const uint32_t* top, float* y, int64_t n,
+                             int exp_bits, int man_bits) {
+  const lpq::FloatParams p = lpq::make_float(exp_bits, man_bits);
+  for (int64_t i = 0; i < n; ++i) {
+    const float xc = fminf(fmaxf(x[i], -p.max_value), p.max_value);
+    y[i] = lpq::quant_float_bits_top(xc, p, top[i], 1u);
+  }
+}
+void hm_quant_float_bits(const float* x, const uint32_t* v, float* y, int64_t n,
+                         int exp_bits, int man_bits) {
+  const lpq::FloatParams p = lpq::make_float(exp_bits, man_bits);
+  for (int64_t i = 0; i < n; ++i) {
+    const float xc = fminf(fmaxf(x[i], -p.max_value), p.max_value);
+    y[i] = lpq::quant_float_bits<0>(xc, p, v[i]);
+  }
+}
 uint64_t hm_stream_key(uint64_t seed, uint64_t call) { return lpq::stream_key(seed, call); }
 }

@@ -37,6 +37,9 @@ def hm():
     L.hm_variates24_balanced.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_fma.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_x4.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_variates24_x4_top.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_quant_float_bits_top.argtypes = [fp, up, fp, C.c_int64, C.c_int, C.c_int]
+    L.hm_quant_float_bits.argtypes = [fp, up, fp, C.c_int64, C.c_int, C.c_int]
     return L
 
 
@@ -102,6 +105,25 @@ def test_float4_variate_form_is_identical(hm):
         hm.hm_variates24(key, base, n, a)
         hm.hm_variates24_x4(key, base, n, b)
         assert np.array_equal(a, b), (key, base)
+        hm.hm_variates24_x4_top(key, base, n, b)
+        assert np.array_equal(a, b), (key, base, "top")
+
+
+@pytest.mark.parametrize("em", [(5, 2), (4, 3), (2, 1), (7, 12), (3, 0), (8, 22)])
+def test_float_bits_top_form_is_identical(hm, em):
+    # quant_float_bits_top(top) == quant_float_bits<stochastic>(top >> 8) for
+    # every sign, whatever the top word's low 8 bits hold
+    rng = np.random.default_rng(em[0] * 31 + em[1])
+    x = inputs(1 << 16, seed=em[0])
+    v = rng.integers(0, 1 << 24, size=x.size, dtype=np.uint64).astype(np.uint32)
+    junk = rng.integers(0, 256, size=x.size, dtype=np.uint64).astype(np.uint32)
+    v[:4] = [0, (1 << 24) - 1, 1, (1 << 23)]
+    top = (v << np.uint32(8)) | junk
+    a = np.empty_like(x)
+    b = np.empty_like(x)
+    hm.hm_quant_float_bits(x, v, a, x.size, *em)
+    hm.hm_quant_float_bits_top(x, top, b, x.size, *em)
+    assert np.array_equal(bits(a), bits(b))
 
 
 @pytest.mark.parametrize("fmt", FORMATS, ids=repr)

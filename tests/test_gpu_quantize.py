@@ -138,10 +138,12 @@ BLOCK_CASES = [
     ((64, 100), 0),         # rows, 128 threads
     ((7, 20000), 0),        # rows, 1024 x 8 float4
     ((5, 40000), 0),        # few long rows -> two-pass segments
-    ((300, 40000), 0),      # cluster plan, 2 CTAs per row, DSMEM max exchange
-    ((80, 200000), 0),      # cluster plan, 4 CTAs per row
-    ((40, 802816), 0),      # ResNet-50 conv1 per-sample block, 8-CTA clusters
-    ((1, 300, 40000), 1),   # cluster plan along dim 1 (leading 1)
+    ((300, 40000), 0),      # chunk rendezvous, 3 chunks per row
+    ((80, 200000), 0),      # chunk rendezvous, 13 chunks per row (ragged last)
+    ((40, 802816), 0),      # ResNet-50 conv1 per-sample block, 49 chunks per row
+    ((1, 300, 40000), 1),   # chunk rendezvous along dim 1 (leading 1)
+    ((2, 65540), 0),        # 5 chunks of 13108 floats (uneven split)
+    ((1 << 20,), None),     # whole tensor, one row of 64 chunks
     ((4096, 64), 0),        # short rows: 16 lanes per row
     ((999, 12), 0),         # short rows: 4 lanes per row
     ((77, 400), 0),         # short rows: 32 lanes x 4 float4
@@ -183,6 +185,55 @@ def test_block_plans_vs_oracle(q, oracle, shape, dim, mode, wl):
     # host path (streamed rows / resident two-pass)
     got_h = q.quantize_fused_at(x, spec_of(q, fmt, mode, seed=77), 3)
     assert same_bits(got_h, want)
+
+
+CLUSTER_CASES = [((300, 40000), 0), ((80, 200000), 0), ((40, 802816), 0), ((6, 1 << 20), 0)]
+
+
+@pytest.mark.parametrize("shape,dim", CLUSTER_CASES, ids=str)
+@pytest.mark.parametrize("mode", ALL_MODES)
+def test_block_rows_without_workspace_take_the_cluster_plan(q, oracle, shape, dim, mode):
+    # lpq_quantize with ws = NULL: the rows of 32K..1M floats that the chunk
+    # plan would take run on the workspace-free cluster plan (DSMEM maxima)
+    import ctypes as C
+    from paper_1910_04540_b200 import _lib
+    rng = np.random.default_rng(hash((shape, mode)) % 2**32)
+    x = rng.uniform(-1, 1, shape).astype(np.float32)
+    x *= (2.0 ** rng.integers(-20, 20, (shape[0], 1))).astype(np.float32)
+    fmt = block_fmt(8, dim)
+    st, want = oracle.quantize(x, fmt, mode, seed=5, call=2)
+    assert st == 0
+    xd = dev(x)
+    y = torch.empty_like(xd)
+    spec = spec_of(q, fmt, mode, seed=5)
+    status = q.quant._status_buf(xd.device)
+    shp = _lib.shape_array(xd.shape)
+    rc = _lib.lib.lpq_quantize(C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()), shp,
+                               xd.dim(), 0, C.byref(spec.format.c()), mode, 5, 2,
+                               C.c_void_p(0), 0, C.c_void_p(status.data_ptr()),
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    q.fetch_status(xd.device)
+    assert same_bits(y, want), (shape, mode)
+
+
+def test_block_chunk_plan_many_rows_and_index_base(q, oracle):
+    # [256, 100352] (ResNet-50 layer-4 activation rows, 7 chunks each) with a
+    # flat-index base that is not a multiple of 4 (scalar variate path), and
+    # rows whose maxima sit in different chunks
+    R, L = 256, 100352
+    x = q.random_uniform((R, L), 11, 0, -1.0, 1.0)
+    for r in range(0, R, 17):
+        x[r, (r * 7919) % L] = 3.0 + r
+    xh = x.cpu().numpy()
+    for mode, base in ((STOCHASTIC, 0), (STOCHASTIC, 6), (NEAREST_EVEN, 3)):
+        spec = q.QuantSpec(q.BlockFloatFormat(8, 0), q.RoundingMode(mode), 21)
+        y = q.quantize_fused_at(x, spec, 1, index_base=base)
+        for r in (0, 17, 100, 255):
+            st, want = oracle.quantize_block_given_max(
+                xh[r:r + 1], block_fmt(8, 0), mode, np.abs(xh[r:r + 1]).max(axis=1),
+                seed=21, call=1, index_base=base + r * L)
+            assert st == 0 and same_bits(y[r:r + 1], want), (mode, base, r)
 
 
 def test_block_columns_grid_y_beyond_65535(q, oracle):
@@ -264,7 +315,7 @@ def test_pass_count_contract(q):
     rng = np.random.default_rng(71)
     cases = [(q.FixedFormat(8, 4), (32, 32), 1), (q.FloatFormat(5, 2), (32, 32), 1),
              (q.BlockFloatFormat(8, 0), (16, 256), 1), (q.BlockFloatFormat(8), (32, 32), 1),
-             (q.BlockFloatFormat(8), (8, 40000), 2), (q.BlockFloatFormat(8, 0), (300, 40000), 1),
+             (q.BlockFloatFormat(8), (8, 40000), 1), (q.BlockFloatFormat(8, 0), (300, 40000), 1),
              (q.BlockFloatFormat(8), (3, 999_999), 2),
              (q.BlockFloatFormat(8, 1), (32, 32), 2)]
     for fmt, shape, passes in cases:
@@ -532,6 +583,7 @@ def test_quantize_file_vs_oracle(q, oracle, tmp_path, fmt, mode, shape):
 
 
 NONFINITE_CASES = [((300, 4096), 0), ((77, 400), 0), ((7, 20000), 0), ((300, 40000), 0),
+                   ((3, 802816), 0), ((1 << 20,), None),
                    ((5, 40000), 0), ((50, 70, 30), 1), ((1_000_003,), None), ((4096, 64), 0)]
 
 
