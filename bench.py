@@ -522,7 +522,10 @@ def run_ours(args, rank, world, local_rank):
 
 # ---------------------------------------------------------------------------
 def run_gemm(args, rank, world, local_rank):
-    """C4: per-op-rounded GEMM 4096^3, float(8,7) after every multiply and add."""
+    """C4: per-op-rounded GEMM 4096^3, float(8,7) after every multiply and add.
+    c4: operands quantized to float(8,7) first, nearest rounding (the
+    hardware-bf16 kernel); c4raw: raw fp32 operands (the FMUL + cvt.rn.bf16x2
+    kernel); c4s: stochastic rounding after every op (the general kernel)."""
     import torch
     import torch.distributed as dist
     import paper_1910_04540_b200 as q
@@ -536,17 +539,19 @@ def run_gemm(args, rank, world, local_rank):
     # and broadcast, outside the timed region
     lo, hi = gemm_rows(M, rank, world)
     f87 = q.QuantSpec(q.FloatFormat(8, 7))
-    a = q.quantize_fused_at(q.random_uniform((hi - lo, K), 41, 0, -1.0, 1.0, device=dev,
-                                             index_base=lo * K), f87, 0)
+    raw = args.config == "c4raw"
+    mode = q.RoundingMode.Stochastic if args.config == "c4s" else q.RoundingMode.NearestEven
+    prep = (lambda t: t) if raw else (lambda t: q.quantize_fused_at(t, f87, 0))
+    a = prep(q.random_uniform((hi - lo, K), 41, 0, -1.0, 1.0, device=dev, index_base=lo * K))
     if rank == 0:
-        b = q.quantize_fused_at(q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev), f87, 0)
+        b = prep(q.random_uniform((K, N), 42, 0, -1.0, 1.0, device=dev))
     else:
         b = torch.empty((K, N), device=dev)
     broadcast_operand(b)
     c = torch.empty((hi - lo, N), device=dev)
     fm = q.FloatFormat(8, 7)
     for _ in range(args.warmup):
-        q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=lo)
+        q.quant_gemm(a, b, fm, fm, mode, 0x5EED, 0, out=c, sync=False, row_base=lo)
     q.fetch_status(dev)
     if world > 1:
         dist.barrier()
@@ -557,7 +562,7 @@ def run_gemm(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         t0.record(s)
         for _ in range(args.steps):
-            q.quant_gemm(a, b, fm, fm, out=c, sync=False, row_base=lo)
+            q.quant_gemm(a, b, fm, fm, mode, 0x5EED, 0, out=c, sync=False, row_base=lo)
         t1.record(s)
         torch.cuda.synchronize()
     q.fetch_status(dev)
@@ -589,7 +594,8 @@ def run_gemm(args, rank, world, local_rank):
             f87o = float_fmt(8, 7)
             t_0 = _t.perf_counter()
             with ThreadPoolExecutor(th) as ex:
-                list(ex.map(lambda r: o.quant_gemm(ah[r:r + 2], bh, f87o, f87o),
+                list(ex.map(lambda r: o.quant_gemm(ah[r:r + 2], bh, f87o, f87o, int(mode),
+                                                   seed=0x5EED, call=0, row_base=r),
                             range(0, rows, 2)))
             secs = _t.perf_counter() - t_0
             cpu = {"value": round(2.0 * rows * N * K / secs / 1e9, 4), "unit": "GFLOP/s",
@@ -607,14 +613,25 @@ def run_gemm(args, rank, world, local_rank):
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32 ops + bf16 rounding",
         "data": "synthetic", "config": {"workload": "C4: 4096x4096x4096, output rows split "
-                                                    "over the GPUs, B broadcast from rank 0",
+                                                    "over the GPUs, B broadcast from rank 0" + {
+                                            "c4": "; float(8,7) operands, nearest",
+                                            "c4raw": "; raw fp32 operands, nearest",
+                                            "c4s": "; float(8,7) operands, stochastic after "
+                                                   "every op"}[args.config],
                                         "rows_per_gpu": hi - lo,
                                         "parallelism": f"rows{world}"},
         "gpu_launches": q.launch_count() - l0,
         "roofline": {"bound": "fp32_cuda_core", "achieved": round(ach, 2),
                      "peak": round(peak_t, 2), "unit": "TFLOP/s",
                      "frac": round(ach / peak_t, 4), "traffic": None,
-                     "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz"},
+                     "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz",
+                     # the bf16 kernels' own bound: an HMUL2/HADD2 (or FMUL
+                     # pair + HADD2) per 64 MACs per warp holds the FMA pipe
+                     # for 4 cycles -> 16 MAC/clk/SMSP (profiles/r02_pipes.md)
+                     "ceiling": None if args.config == "c4s" else {
+                         "value": round(sms * 4 * 16 * 2 * 1.965e9 / 1e12, 2),
+                         "unit": "TFLOP/s", "frac": round(ach / (sms * 4 * 16 * 2 * 1.965e9 / 1e12), 4),
+                         "what": "bf16x2 FMA-pipe issue bound (HMUL2 + HADD2 per 2 MACs)"}},
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }
 
@@ -860,23 +877,26 @@ def run_reference(args, rank, world):
         config = {"workload": cfg["workload"], "elements_per_gpu": n,
                   "format": "%s:%d:%d" % cfg["fmt"], "rounding": cfg["mode"],
                   "parallelism": "host threads"}
-    elif args.config in ("c4", "c4ref"):
+    elif args.config in ("c4", "c4raw", "c4s", "c4ref"):
         from oracle_lib import Oracle, fixed_fmt, float_fmt
         from concurrent.futures import ThreadPoolExecutor
-        rows = 2 * th if args.config == "c4" else 32
+        rows = 2 * th if args.config != "c4ref" else 32
         a = ref.random_uniform((rows, 4096), 41, 0, -1.0, 1.0)
         b = ref.random_uniform((4096, 4096), 42, 0, -1.0, 1.0)
-        if args.config == "c4":
+        if args.config != "c4ref":
             o = Oracle()
             f87 = float_fmt(8, 7)
-            _, a = ref.quantize(a, f87, 1)
-            _, b = ref.quantize(b, f87, 1)
+            gmode = 0 if args.config == "c4s" else 1
+            if args.config != "c4raw":
+                _, a = ref.quantize(a, f87, 1)
+                _, b = ref.quantize(b, f87, 1)
             kind = "port"
 
             def one():
                 t0 = time.perf_counter()
                 with ThreadPoolExecutor(th) as ex:
-                    list(ex.map(lambda r: o.quant_gemm(a[r:r + 2], b, f87, f87),
+                    list(ex.map(lambda r: o.quant_gemm(a[r:r + 2], b, f87, f87, gmode,
+                                                       seed=0x5EED, call=0, row_base=r),
                                 range(0, rows, 2)))
                 return time.perf_counter() - t0
             sample = (f"{rows} of the 4096 output rows per step through the restated per-op "
@@ -946,7 +966,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c4ref", "c5"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c4raw", "c4s", "c4ref", "c5"])
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="capture the timed steps in a CUDA graph (auto: steps "
                          "moving < 1 GiB, which are launch-bound from Python)")
@@ -991,7 +1011,8 @@ def main():
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    runner = {"c4": run_gemm, "c4ref": run_matmul_q, "c5": run_sweep}.get(args.config, run_ours)
+    runner = {"c4": run_gemm, "c4raw": run_gemm, "c4s": run_gemm, "c4ref": run_matmul_q,
+              "c5": run_sweep}.get(args.config, run_ours)
     out = runner(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)

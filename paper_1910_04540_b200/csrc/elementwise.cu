@@ -4,10 +4,12 @@
 // Replaces the per-element CPU loops fused_fixed / fused_float
 // (proj/src/quant_ops.cpp:33-66) driven by quant_pass/parallel_for
 // (quant_ops.cpp:13-31, tensor.cpp:118-136).  HBM-bound: 8 algorithmic bytes
-// per element.  Each thread moves U float4 per trip with the loads issued
-// before any arithmetic (U*16 B in flight per thread), streaming cache hints
-// (ld.global.cs / st.global.cs), and a grid sized to the resident-CTA count
-// of the 148 SMs, looping grid-stride.
+// per element.  Each thread moves U float4 with the loads issued before any
+// arithmetic (U*16 B in flight per thread) and streaming cache hints
+// (ld.global.cs / st.global.cs); the grid covers the tensor in one trip per
+// thread (launch_ew: U = 8 for large tensors, 4-7 below 2^26 elements so the
+// last wave of 4 CTAs/SM fills well), the kernel loops grid-stride only when
+// the grid would exceed the launch limit.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/lpq.h"
@@ -111,6 +112,28 @@ __device__ __forceinline__ bool bf16_path_ok(const GemmScan& s, int64_t K) {
   return lg < 126.0;
 }
 
+// Raw (not bf16-exact) fp32 operands under Qm = Qa = float(8,7) nearest:
+// fl32(a*b) is the reference's product, and Qm of it is cvt.rn.bf16 when it
+// is normal; the sums are of bf16 values, so HADD2.BF16 (one rounding of the
+// exact sum) equals Qa(fl32(sum)) as in the exact path.  Every nonzero
+// operand normal and every value a multiple of G = 2^(ea_min + eb_min - 7)
+// >= 2^-126 keeps every nonzero product and sum normal; the overflow bound
+// is the exact path's.
+__device__ __forceinline__ bool bf16raw_path_ok(const GemmScan& s, int64_t K) {
+  if (s.nonfinite) return false;
+  if (s.a_min_nz_exp_field == 0 || s.b_min_nz_exp_field == 0)
+    return true;  // A or B is all zeros: every product and sum is +-0
+  const int fa = 255 - (int)s.a_min_nz_exp_field, fb = 255 - (int)s.b_min_nz_exp_field;
+  if (fa == 0 || fb == 0) return false;  // a subnormal operand
+  const int ea_min = fa - 127, eb_min = fb - 127;
+  const int ea_max = (int)s.a_max_exp_field - 127;
+  const int eb_max = (int)s.b_max_exp_field - 127;
+  if (ea_min + eb_min - 7 < -126) return false;
+  const double lg = log2((double)K) + (ea_max + 1) + (eb_max + 1) +
+                    (double)(K + 1) * 0.00563 + 1.0;
+  return lg < 126.0;
+}
+
 // ---------------------------------------------------------------------------
 // k_qgemm_bf16: 128x128 CTA tile, 128 threads, 8x16 outputs per thread held
 // as 64 bf16x2 accumulators; K staged 16 at a time into double-buffered
@@ -150,14 +173,28 @@ __device__ __forceinline__ float4 ld_tile4(const float* __restrict__ p,
   return v;
 }
 
-template <bool VEC>
+__device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// RAW: operands that are not bf16-exact (bf16raw_path_ok): fp32 tiles in
+// shared memory, each product an FMUL pair rounded by one F2FP (ALU pipe)
+// into a bf16x2 word, then HADD2 -- the same FMA-pipe cycles per MAC as the
+// HMUL2 form (measured: an HMUL2/HADD2 occupies both FMA half-pipes, an FMUL
+// one), so raw operands run at the exact path's rate.
+template <bool VEC, bool RAW>
 __global__ void __launch_bounds__(kQT)
     k_qgemm_bf16(const float* __restrict__ A, const float* __restrict__ B,
                  float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                  const GemmScan* __restrict__ scan) {
-  if (!bf16_path_ok(*scan, K)) return;  // the general kernel runs instead
-  __shared__ __align__(16) uint16_t As[2][kBK][kBM];
-  __shared__ __align__(16) uint16_t Bs[2][kBK][kBN];
+  if (RAW ? (bf16_path_ok(*scan, K) || !bf16raw_path_ok(*scan, K))
+          : !bf16_path_ok(*scan, K))
+    return;  // another kernel of the launch runs instead
+  using Elem = typename std::conditional<RAW, float, uint16_t>::type;
+  __shared__ __align__(16) Elem As[2][kBK][kBM];
+  __shared__ __align__(16) Elem Bs[2][kBK][kBN];
   const int t = threadIdx.x;
   const int tx = t & 7, ty = t >> 3;  // 8 column groups x 16 row groups
   const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
@@ -183,16 +220,24 @@ __global__ void __launch_bounds__(kQT)
     for (int i = 0; i < 4; ++i) {
       const int f = t + kQT * i;
       const int row = f >> 2, kq = (f & 3) * 4;
-      As[buf][kq + 0][row] = (uint16_t)(f2u(ra[i].x) >> 16);
-      As[buf][kq + 1][row] = (uint16_t)(f2u(ra[i].y) >> 16);
-      As[buf][kq + 2][row] = (uint16_t)(f2u(ra[i].z) >> 16);
-      As[buf][kq + 3][row] = (uint16_t)(f2u(ra[i].w) >> 16);
       const int g = t + kQT * i;
       const int kr = g >> 5, col = (g & 31) * 4;
-      uint2 w;
-      w.x = (f2u(rb[i].x) >> 16) | (f2u(rb[i].y) & 0xFFFF0000u);
-      w.y = (f2u(rb[i].z) >> 16) | (f2u(rb[i].w) & 0xFFFF0000u);
-      *reinterpret_cast<uint2*>(&Bs[buf][kr][col]) = w;
+      if constexpr (RAW) {
+        As[buf][kq + 0][row] = ra[i].x;
+        As[buf][kq + 1][row] = ra[i].y;
+        As[buf][kq + 2][row] = ra[i].z;
+        As[buf][kq + 3][row] = ra[i].w;
+        *reinterpret_cast<float4*>(&Bs[buf][kr][col]) = rb[i];
+      } else {
+        As[buf][kq + 0][row] = (uint16_t)(f2u(ra[i].x) >> 16);
+        As[buf][kq + 1][row] = (uint16_t)(f2u(ra[i].y) >> 16);
+        As[buf][kq + 2][row] = (uint16_t)(f2u(ra[i].z) >> 16);
+        As[buf][kq + 3][row] = (uint16_t)(f2u(ra[i].w) >> 16);
+        uint2 w;
+        w.x = (f2u(rb[i].x) >> 16) | (f2u(rb[i].y) & 0xFFFF0000u);
+        w.y = (f2u(rb[i].z) >> 16) | (f2u(rb[i].w) & 0xFFFF0000u);
+        *reinterpret_cast<uint2*>(&Bs[buf][kr][col]) = w;
+      }
     }
   };
 
@@ -205,6 +250,27 @@ __global__ void __launch_bounds__(kQT)
     if (kt + 1 < nk) load((kt + 1) * kBK);
     const int kk_end = (int)min((int64_t)kBK, K - kt * kBK);
     auto step = [&](int kk) {
+      if constexpr (RAW) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
+        float bf[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 16 + 4 * q]);
+          bf[4 * q] = b4.x;
+          bf[4 * q + 1] = b4.y;
+          bf[4 * q + 2] = b4.z;
+          bf[4 * q + 3] = b4.w;
+        }
+        const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            acc[i][j] = badd2(acc[i][j], cvt_bf16x2(fmul(af[i], bf[2 * j + 1]),
+                                                    fmul(af[i], bf[2 * j])));
+        return;
+      }
       const uint4 av = *reinterpret_cast<const uint4*>(&As[buf][kk][ty * 8]);
       const uint4 b0 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16]);
       const uint4 b1 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16 + 8]);
@@ -280,7 +346,8 @@ __global__ void __launch_bounds__(kGT)
       atomicOr(status, kStatusNonFinite);
     return;
   }
-  if (!ALWAYS && bf16_path_ok(*scan, K)) return;  // the bf16 kernel did it
+  if (!ALWAYS && (bf16_path_ok(*scan, K) || bf16raw_path_ok(*scan, K)))
+    return;  // a bf16 kernel did it
   __shared__ float As[kGK][kGM];
   __shared__ float Bs[kGK][kGN];
   __shared__ uint64_t keys[kGK][2];
@@ -608,13 +675,18 @@ cudaError_t launch_quant_gemm(const float* A, const float* B, float* C,
     note_launch();
   }
   const bool try_bf16 = bf16_formats && mode == kNearestEven;
-  if (try_bf16) {
+  if (try_bf16) {  // exact bf16 operands, else raw fp32 ones (one of them runs)
     dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)((M + kBM - 1) / kBM));
     const bool vec = (K % 4 == 0) && (N % 4 == 0) && aligned16(A) &&
                      aligned16(B) && aligned16(C);
-    if (vec) k_qgemm_bf16<true><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
-    else k_qgemm_bf16<false><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
-    note_launch();
+    if (vec) {
+      k_qgemm_bf16<true, false><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
+      k_qgemm_bf16<true, true><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
+    } else {
+      k_qgemm_bf16<false, false><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
+      k_qgemm_bf16<false, true><<<grid, kQT, 0, s>>>(A, B, C, M, N, K, scan);
+    }
+    note_launch(2);
   }
   switch (mode) {
     case kStochastic: launch_general<kStochastic>(A, B, C, M, N, K, row_base, qm, qa, !try_bf16, seed, call, scan, status, s); break;

@@ -18,6 +18,8 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -62,10 +64,6 @@ struct HostCtx {
   uint32_t* daux = nullptr;  // device: encode flag
   uint32_t* paux = nullptr;  // page-locked: block maxima [extent] + flag
   int64_t paux_cap = 0;
-  // direct pipeline: per part, "copied in" and "codes back" events
-  static constexpr int kParts = 8;
-  cudaEvent_t ev_in[kParts] = {};
-  cudaEvent_t ev_out[kParts] = {};
   uint32_t* pstatus = nullptr;  // page-locked status word (status fetch)
   std::mutex mu;
 
@@ -99,11 +97,6 @@ struct HostCtx {
     if (paux) cudaFreeHost(paux);
     if (pstatus) cudaFreeHost(pstatus);
     pstatus = nullptr;
-    for (int k = 0; k < kParts; ++k) {
-      if (ev_in[k]) cudaEventDestroy(ev_in[k]);
-      if (ev_out[k]) cudaEventDestroy(ev_out[k]);
-      ev_in[k] = ev_out[k] = nullptr;
-    }
     pstage = nullptr;
     dcodef = nullptr;
     pcodef = nullptr;
@@ -122,11 +115,6 @@ struct HostCtx {
       cudaError_t e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
       if (e != cudaSuccess) return e;
       e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    for (int k = 0; k < kParts; ++k) {
-      cudaError_t e = cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
       if (e != cudaSuccess) return e;
     }
     cudaError_t e = cudaMallocHost(&pstatus, sizeof(uint32_t));
@@ -276,6 +264,8 @@ struct Decode {
 // cost more than a 4 MB copy).  Parts of >= 512 KB, at most 16 threads
 // including the caller.
 class CopyPool {
+  struct Job;
+
  public:
   static CopyPool& get() {
     static CopyPool pool;
@@ -290,14 +280,23 @@ class CopyPool {
            const Decode* dec = nullptr, size_t first = 0) {
     const size_t dst_unit = dec ? sizeof(float) : 1;
     const size_t part = (count / parts + 63) & ~size_t(63);
-    std::unique_lock<std::mutex> lk(mu_);
-    jobs_.clear();
-    for (int t = 1; t < parts; ++t) {
+    std::vector<Job> jobs;
+    for (int t = 0; t < parts; ++t) {
       const size_t b = part * t;
       if (b >= count) break;
-      jobs_.push_back(Job{dst + b * dst_unit, src + b, std::min(part, count - b), dec,
-                          first + b});
+      jobs.push_back(Job{dst + b * dst_unit, src + b, std::min(part, count - b), dec,
+                         first + b});
     }
+    run_list(std::move(jobs));
+  }
+
+ private:
+  // jobs[0] runs on the caller, the rest on whichever thread takes them
+  void run_list(std::vector<Job>&& all) {
+    if (all.empty()) return;
+    const Job first_job = all[0];
+    std::unique_lock<std::mutex> lk(mu_);
+    jobs_.assign(all.begin() + 1, all.end());
     next_ = 0;
     pending_ = jobs_.size();
     apending_.store(pending_, std::memory_order_release);
@@ -305,7 +304,7 @@ class CopyPool {
     agen_.store(gen_, std::memory_order_release);
     lk.unlock();
     cv_.notify_all();
-    exec(Job{dst, src, std::min(part, count), dec, first});
+    exec(first_job);
     lk.lock();
     // help with whatever the workers have not picked up, then wait
     while (next_ < jobs_.size()) {
@@ -324,7 +323,6 @@ class CopyPool {
     done_.wait(lk, [&] { return pending_ == 0; });
   }
 
- private:
   struct Job {
     char* dst;
     const char* src;
@@ -377,6 +375,9 @@ class CopyPool {
     const auto t0 = std::chrono::steady_clock::now();
     for (int i = 0;; ++i) {
       if (pred()) return true;
+#if defined(__x86_64__)
+      __builtin_ia32_pause();  // leave the core's issue slots to its sibling
+#endif
       if ((i & 63) == 63 &&
           std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200))
         return false;
@@ -546,6 +547,8 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
   ByteCode bc{};
   float lut[256];
   const bool coded = !rows && byte_code_for(f, mode, &bc, lut);
+  note_passes(1);   // one data pass for the whole call:
+  PassScope scope;  // the chunks' device calls do not count again
   const Decode dec = coded ? decoder_for(f, bc, lut) : Decode{};
   auto finish = [&](int64_t ci) {
     const int k = (int)(ci % kStreams);
@@ -675,16 +678,15 @@ lpq_status d2h_small_and_fetch(HostCtx* c, float* y, const float* d, int64_t n,
   return LPQ_OK;
 }
 
-// Small tensors (<= 16 MB).  Formats whose every quantized value has a
-// one-byte code (ByteCode: fixed wl <= 8 saturating, float 1 + exp + man <=
-// 8) run as a pipeline of up to kParts parts over two streams: the input is
-// staged once (pool memcpy into page-locked memory), then part k's H2D copy
-// (stream 0) overlaps part k-1's kernels and code copy-back (stream 1, on
-// the other copy engine), and the host decodes part k-1 while part k is in
-// flight.  A quarter of the device->host bytes cross PCIe, decoded
-// bit-exactly on the host.  Block formats with wl <= 8 whose plan leaves the
-// block maxima in the workspace also copy codes back (decoded with each
-// block's step); everything else copies fp32.
+// Small tensors (<= 16 MB): one staged copy in, the device call, one copy
+// out on one stream.  Formats whose every quantized value has a one-byte code
+// (ByteCode: fixed wl <= 8 saturating, float 1 + exp + man <= 8; block wl <=
+// 8 on the plans that leave the block maxima in the workspace) copy the codes
+// back instead of fp32 -- a quarter of the device->host bytes, decoded
+// bit-exactly on the host by the copy pool.  (Pipelining the call in parts
+// over two streams was measured on the B200 host, scripts/host_crit7.cpp:
+// the part's H2D and the previous part's D2H complete together -- the copies
+// do not overlap here -- so 2..8 parts only added ~15 us of API calls each.)
 lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
                            const int64_t* shape, int rank, int64_t n,
                            uint64_t index_base, const lpq_format* f, int mode,
@@ -696,58 +698,6 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
   ByteCode bc{};
   float lut[256];
   const bool coded = byte_code_for(f, mode, &bc, lut);
-  if (coded && f->kind != LPQ_BLOCK) {
-    // validate once (the parts' device calls see 1-D pieces)
-    lpq_status st = check_format(f);
-    if (st != LPQ_OK) return st;
-    LPQ_TRY(c->ensure_codes(n, 1));
-    const int64_t parts = std::max<int64_t>(
-        1, std::min<int64_t>(HostCtx::kParts, n / (int64_t(1) << 17)));
-    const int64_t part = ((n + parts - 1) / parts + 1023) / 1024 * 1024;
-    const float* src = x;
-    if (!is_pinned(x)) {
-      LPQ_TRY(c->ensure_stage(n));
-      parallel_memcpy(c->pstage, x, sizeof(float) * (size_t)n, size_t(256) << 10);
-      src = c->pstage;
-    }
-    cudaStream_t s1 = c->st[1];
-    const Decode dec = decoder_for(f, bc, lut);
-    lpq_status qst = LPQ_OK;
-    int64_t issued = 0;
-    {
-      PassScope scope;  // one data pass for the whole call, counted below
-      for (int64_t k = 0, off = 0; off < n; ++k, off += part) {
-        const int64_t len = std::min(part, n - off);
-        LPQ_TRY(cudaMemcpyAsync(c->dfull + off, src + off, sizeof(float) * (size_t)len,
-                                cudaMemcpyHostToDevice, s));
-        LPQ_TRY(cudaEventRecord(c->ev_in[k], s));
-        LPQ_TRY(cudaStreamWaitEvent(s1, c->ev_in[k], 0));
-        const int64_t shp[1] = {len};
-        qst = quantize_device(c->dfull + off, c->dfull + off, shp, 1, index_base + (uint64_t)off,
-                              f, mode, seed, call, nullptr, 0, c->d_status, s1);
-        if (qst != LPQ_OK) break;
-        LPQ_TRY(launch_encode8(c->dfull + off, c->dcodef + off, len, bc, s1));
-        LPQ_TRY(cudaMemcpyAsync(c->pcodef + off, c->dcodef + off, (size_t)len,
-                                cudaMemcpyDeviceToHost, s1));
-        LPQ_TRY(cudaEventRecord(c->ev_out[k], s1));
-        ++issued;
-      }
-    }
-    note_passes(1);
-    if (qst != LPQ_OK) {
-      cudaStreamSynchronize(s);
-      cudaStreamSynchronize(s1);
-      return qst;
-    }
-    // decode part by part as the codes land (statuses are checked at the
-    // end: a flagged call discards its output, like the reference's throw)
-    for (int64_t k = 0; k < issued; ++k) {
-      const int64_t off = k * part, len = std::min(part, n - off);
-      LPQ_TRY(cudaEventSynchronize(c->ev_out[k]));
-      parallel_decode(y + off, c->pcodef + off, (size_t)len, dec);
-    }
-    return c->fetch_status(s1);
-  }
   LPQ_TRY(h2d_small(c, c->dfull, x, n, s));
   const lpq_status qst = quantize_device(c->dfull, c->dfull, shape, rank, index_base,
                                          f, mode, seed, call, c->ws, c->ws_bytes,
@@ -755,6 +705,15 @@ lpq_status direct_quantize(HostCtx* c, const float* x, float* y,
   if (qst != LPQ_OK) {
     cudaStreamSynchronize(s);
     return qst;
+  }
+  if (coded) {
+    LPQ_TRY(c->ensure_codes(n, 1));
+    LPQ_TRY(launch_encode8(c->dfull, c->dcodef, n, bc, s));
+    LPQ_TRY(cudaMemcpyAsync(c->pcodef, c->dcodef, (size_t)n, cudaMemcpyDeviceToHost, s));
+    const lpq_status st = c->fetch_status(s);
+    if (st != LPQ_OK) return st;
+    parallel_decode(y, c->pcodef, (size_t)n, decoder_for(f, bc, lut));
+    return LPQ_OK;
   }
   BlockGeom g{1, 1, n};
   bool bcoded = false;

@@ -61,6 +61,43 @@ def test_quant_gemm_general_path_non_bf16_inputs(q, oracle):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
 
 
+@pytest.mark.parametrize("M,N,K,seed", [(70, 50, 90, 4), (128, 128, 64, 5), (131, 257, 129, 6),
+                                        (1, 3, 2, 7), (256, 128, 1000, 8)])
+def test_quant_gemm_raw_fp32_operands(q, oracle, M, N, K, seed):
+    # operands that are NOT bf16-exact (float(8,7) nearest): the raw kernel
+    # (FMUL pairs rounded by cvt.rn.bf16x2, then HADD2) under the pre-scan
+    # proof; zeros of both signs included
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(-3, 3, (M, K)).astype(np.float32)
+    b = rng.uniform(-3, 3, (K, N)).astype(np.float32)
+    a.reshape(-1)[:: 7] = 0.0
+    b.reshape(-1)[1:: 11] = -0.0
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    assert st == 0
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("case", ["tiny", "subnormal", "huge"])
+def test_quant_gemm_raw_guards(q, oracle, case):
+    # raw operands outside the raw kernel's proof: products near 2^-126, a
+    # subnormal operand, sums near the top of the range -> the general kernel
+    rng = np.random.default_rng(17)
+    a = rng.uniform(-1, 1, (40, 60)).astype(np.float32)
+    b = rng.uniform(-1, 1, (60, 30)).astype(np.float32)
+    if case == "tiny":
+        a *= np.float32(2.0**-60)
+        b *= np.float32(2.0**-58)
+    elif case == "subnormal":
+        a[3, 5] = np.float32(2.0**-140)
+    else:
+        a *= np.float32(2.0**66)
+        b *= np.float32(2.0**60)
+    st, want = oracle.quant_gemm(a, b, float_fmt(8, 7), float_fmt(8, 7))
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(8, 7), q.FloatFormat(8, 7))
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want)), case
+
+
 def test_quant_gemm_underflow_guard(q, oracle):
     # bf16-exact operands whose products fall below 2^-126: the device-side
     # pre-scan must route to the general kernel (two-point underflow grid)
