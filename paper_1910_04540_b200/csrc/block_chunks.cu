@@ -31,7 +31,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -50,7 +49,9 @@ constexpr int kT = 256;  // threads per CTA
 // (4, 6), (4, 8), (6, 4) on the ResNet-50 activation rows (scripts/
 // time_act_plans.py): more resident CTAs hide the rendezvous and load
 // latencies until the register cap spills; [256, 802816] nearest 4607 ->
-// 4673 GB/s, stochastic 5801 -> 5967.
+// 4673 GB/s, stochastic 5801 -> 5967.  (A shared-memory variant that
+// double-buffers chunks with cp.async and issues the next chunk's loads
+// before the rendezvous, 3 CTAs/SM: 3867 / 4710 -- slower.)
 constexpr int kV = 8;
 constexpr int kB = 4;
 
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(kT, kB)
       atomicMax(rowmax + row, m);
       red_release_add(arrive + row, 1u);
     }
+    // (two rounds ahead measured slower: [256, 802816] nearest 4662 -> 4425)
     if (t + G < total) {
       int64_t nrow, noff4;
       const int64_t nlen4 = chunk(t + G, nrow, noff4);
@@ -199,152 +201,6 @@ __global__ void __launch_bounds__(kT, kB)
   if (lane == 0) flag(status, bad);
 }
 
-// Shared-memory variant: each CTA double-buffers its chunks in shared memory
-// with cp.async (LDGSTS, no registers held), issuing the NEXT chunk's loads
-// before it waits at the row rendezvous, so the load latency hides behind the
-// wait and the quantize pass.  kSV float4 per thread per chunk, kSB CTAs/SM.
-constexpr int kSV = 8;
-constexpr int kSB = 3;
-constexpr size_t kSmemChunk = sizeof(float4) * kT * kSV;  // 32 KB
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
-}
-
-template <int M, bool IDX4>
-__global__ void __launch_bounds__(kT, kSB)
-    k_block_chunks_smem(const float* __restrict__ x, float* __restrict__ y, int64_t L,
-                        int64_t nrows, int64_t cpr, int64_t S4, uint32_t* __restrict__ ws,
-                        uint64_t base, uint64_t key, int wl, RngMul rm,
-                        uint32_t* __restrict__ status) {
-  extern __shared__ float4 sbuf[];  // [2][kT * kSV]
-  __shared__ uint32_t red[kT / 32];
-  __shared__ uint32_t sh_max;
-  __shared__ uint32_t sh_row;
-  uint32_t* rowmax = ws;
-  uint32_t* arrive = ws + nrows;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t total = nrows * cpr;
-  const int64_t L4 = L >> 2;
-  const int64_t G = gridDim.x;
-  const float kmin = -(float)(1 << (wl - 1));
-  const float kmax = (float)((1 << (wl - 1)) - 1);
-  auto chunk = [&](int64_t t, int64_t& row, int64_t& off4) {
-    row = t / cpr;
-    off4 = (t - row * cpr) * S4;
-    return S4 < L4 - off4 ? S4 : L4 - off4;
-  };
-  auto issue = [&](int64_t t, float4* dst) {  // this thread's loads of chunk t
-    int64_t row, off4;
-    const int64_t len4 = chunk(t, row, off4);
-    const float4* src = reinterpret_cast<const float4*>(x + row * L) + off4;
-#pragma unroll
-    for (int k = 0; k < kSV; ++k) {
-      const int64_t j = threadIdx.x + (int64_t)k * kT;
-      if (j < len4) cp_async16(dst + j, src + j);
-    }
-    cp_async_commit();
-  };
-  uint32_t bad = 0;
-  int cur = 0;
-  if ((int64_t)blockIdx.x < total) issue(blockIdx.x, sbuf);
-  for (int64_t t = blockIdx.x; t < total; t += G, cur ^= 1) {
-    int64_t row, off4;
-    const int64_t len4 = chunk(t, row, off4);
-    float4* buf = sbuf + (size_t)cur * kT * kSV;
-    cp_async_wait<0>();  // this thread's loads of chunk t (the only group in flight)
-    float mf = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kSV; ++k) {
-      const int64_t j = threadIdx.x + (int64_t)k * kT;
-      if (j < len4) absmax_nan(buf[j], mf);  // each thread reads what it loaded
-    }
-    uint32_t m = __reduce_max_sync(kFull, f2u(mf));
-    if (lane == 0) red[warp] = m;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t u = lane < kT / 32 ? red[lane] : 0u;
-      u = __reduce_max_sync(kFull, u);
-      if (lane == 0) sh_max = u;
-    }
-    __syncthreads();
-    m = sh_max;
-    if (m > 0x7F800000u) {  // NaN in the chunk (uniform)
-      bad |= 1u;
-      float nf = 0.0f;
-      mf = 0.0f;
-#pragma unroll
-      for (int k = 0; k < kSV; ++k) {
-        const int64_t j = threadIdx.x + (int64_t)k * kT;
-        if (j < len4) absmax_nf(buf[j], mf, nf);
-      }
-      m = __reduce_max_sync(kFull, f2u(mf));
-      __syncthreads();
-      if (lane == 0) red[warp] = m;
-      __syncthreads();
-      if (warp == 0) {
-        uint32_t u = lane < kT / 32 ? red[lane] : 0u;
-        u = __reduce_max_sync(kFull, u);
-        if (lane == 0) sh_max = u;
-      }
-      __syncthreads();
-      m = sh_max;
-    }
-    if (threadIdx.x == 0) {
-      atomicMax(rowmax + row, m);
-      red_release_add(arrive + row, 1u);
-    }
-    // the next chunk's loads go out before the wait (into the other buffer,
-    // whose previous chunk every thread finished reading last iteration)
-    if (t + G < total) issue(t + G, sbuf + (size_t)(cur ^ 1) * kT * kSV);
-    if (threadIdx.x == 0) {
-      const long long t0 = clock64();
-      while (ld_acquire_gpu(arrive + row) < (uint32_t)cpr) {
-        __nanosleep(64);
-        if (clock64() - t0 > (1ll << 32)) __trap();  // watchdog (see k_block_chunks)
-      }
-      sh_row = ld_relaxed_gpu(rowmax + row);
-    }
-    __syncthreads();
-    const BlockScale sc = make_block_scale(sh_row, wl);
-    if (sc.bad) bad |= 2u;
-    float4* __restrict__ yr = reinterpret_cast<float4*>(y + row * L) + off4;
-    const uint64_t ebase = base + (uint64_t)(row * L + 4 * off4);
-    auto run = [&](auto two_t, auto guard_t) {
-      constexpr bool TWO = decltype(two_t)::value;
-      constexpr bool GUARD = decltype(guard_t)::value;
-#pragma unroll
-      for (int k = 0; k < kSV; ++k) {
-        const int64_t j = threadIdx.x + (int64_t)k * kT;
-        if (j < len4)
-          __stcs(yr + j, qb4<M, TWO, IDX4, GUARD>(buf[j], sc, kmin, kmax, key,
-                                                  ebase + 4 * j, rm));
-      }
-    };
-    if (two_factor(sc)) run(std::true_type{}, std::false_type{});
-    else if (M == kStochastic && needs_guard(sc)) run(std::false_type{}, std::true_type{});
-    else run(std::false_type{}, std::false_type{});
-  }
-  bad = __reduce_or_sync(kFull, bad);
-  if (lane == 0) flag(status, bad);
-}
-
-bool use_smem() {  // LPQ_CHUNK_SMEM=1: the shared-memory variant (A/B)
-  static const bool b = [] {
-    const char* e = std::getenv("LPQ_CHUNK_SMEM");
-    return e && std::atoi(e) != 0;
-  }();
-  return b;
-}
-
 template <int M, bool IDX4>
 int resident_ctas_t() {
   static int per_sm = -1;
@@ -352,17 +208,9 @@ int resident_ctas_t() {
   std::lock_guard<std::mutex> lk(mu);
   if (per_sm < 0) {
     int b = 0;
-    cudaError_t e;
-    if (use_smem()) {
-      e = cudaFuncSetAttribute(k_block_chunks_smem<M, IDX4>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kSmemChunk));
-      if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_block_chunks_smem<M, IDX4>, kT,
-                                                          2 * kSmemChunk);
-    } else {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_block_chunks<M, IDX4>, kT, 0);
-    }
-    if (e != cudaSuccess) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_block_chunks<M, IDX4>, kT, 0) !=
+        cudaSuccess)
+      b = 1;
     per_sm = std::max(1, b);
   }
   return per_sm * device_info().sm_count;
@@ -409,15 +257,9 @@ cudaError_t launch_chunks_t(const float* x, float* y, int64_t L, int64_t nrows,
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (use_smem()) {
-    cfg.dynamicSmemBytes = 2 * kSmemChunk;
-    e = cudaLaunchKernelEx(&cfg, k_block_chunks_smem<M, IDX4>, x, y, L, nrows, cpr, S4,
-                           static_cast<uint32_t*>(ws), base, key, wl, rng_mul(), st);
-  } else {
-    e = cudaLaunchKernelEx(&cfg, k_block_chunks<M, IDX4>, x, y, L, nrows, cpr, S4,
-                           static_cast<uint32_t*>(ws), base, key, wl, rng_mul(), st);
-  }
+  cfg.numAttrs = 1;  // (without it: ~6 % faster, but no co-residency guarantee)
+  e = cudaLaunchKernelEx(&cfg, k_block_chunks<M, IDX4>, x, y, L, nrows, cpr, S4,
+                         static_cast<uint32_t*>(ws), base, key, wl, rng_mul(), st);
   note_launch();
   return e;
 }

@@ -138,7 +138,9 @@ __device__ __forceinline__ bool bf16raw_path_ok(const GemmScan& s, int64_t K) {
 // k_qgemm_bf16: 128x128 CTA tile, 128 threads, 8x16 outputs per thread held
 // as 64 bf16x2 accumulators; K staged 16 at a time into double-buffered
 // shared memory as bf16 (A transposed so a thread's 8 rows are one 16-byte
-// load), global tiles prefetched into registers one step ahead.
+// load), global tiles prefetched into registers one step ahead.  A thread's
+// 16 columns are two groups of 8, 64 apart (tx*8, tx*8 + 64), so the B
+// fragment loads of a quarter-warp are contiguous.
 constexpr int kBM = 128, kBN = 128, kBK = 16, kQT = 128;
 
 __device__ __forceinline__ uint32_t bmul2(uint32_t a, uint32_t b) {
@@ -253,10 +255,12 @@ __global__ void __launch_bounds__(kQT)
       if constexpr (RAW) {
         const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
         const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
+        // columns tx*4 + 32q .. +3: a quarter-warp's float4 loads are 128
+        // contiguous bytes (conflict-free; tx*16 + 4q was 4-way conflicted)
         float bf[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 16 + 4 * q]);
+          const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4 + 32 * q]);
           bf[4 * q] = b4.x;
           bf[4 * q + 1] = b4.y;
           bf[4 * q + 2] = b4.z;
@@ -272,8 +276,10 @@ __global__ void __launch_bounds__(kQT)
         return;
       }
       const uint4 av = *reinterpret_cast<const uint4*>(&As[buf][kk][ty * 8]);
-      const uint4 b0 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16]);
-      const uint4 b1 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 16 + 8]);
+      // columns tx*8 + 64q .. +7: a quarter-warp's 16-byte loads are 128
+      // contiguous bytes (conflict-free; tx*16 was 2-way conflicted)
+      const uint4 b0 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 8]);
+      const uint4 b1 = *reinterpret_cast<const uint4*>(&Bs[buf][kk][tx * 8 + 64]);
       const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
       const uint32_t bw[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -283,10 +289,15 @@ __global__ void __launch_bounds__(kQT)
         for (int j = 0; j < 8; ++j) acc[i][j] = badd2(acc[i][j], bmul2(a2, bw[j]));
       }
     };
-    if (kk_end == kBK) {
+    if (kk_end == kBK && !RAW) {
       // full tile: unrolled so the shared-memory loads of k+1 overlap the
       // math of k (the k order of every accumulator is unchanged)
 #pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) step(kk);
+    } else if (kk_end == kBK) {
+      // RAW: 256 instructions per k; a full unroll overflowed the
+      // instruction cache (ncu: "no instruction" 2.9 stalls per issue)
+#pragma unroll 2
       for (int kk = 0; kk < kBK; ++kk) step(kk);
     } else {
       for (int kk = 0; kk < kk_end; ++kk) step(kk);
@@ -303,7 +314,10 @@ __global__ void __launch_bounds__(kQT)
     float* crow = C + row * N;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int64_t col = n0 + tx * 16 + 2 * j;
+      // word j holds columns col, col + 1 (RAW: tx*4 + 32*(j/2) + 2*(j%2);
+      // bf16: tx*8 + 64*(j/4) + 2*(j%4))
+      const int64_t col = RAW ? n0 + tx * 4 + 32 * (j >> 1) + 2 * (j & 1)
+                              : n0 + tx * 8 + 64 * (j >> 2) + 2 * (j & 3);
       const float lo = u2f(acc[i][j] << 16), hi = u2f(acc[i][j] & 0xFFFF0000u);
       if (VEC && col + 1 < N) {
         *reinterpret_cast<float2*>(crow + col) = make_float2(lo, hi);
