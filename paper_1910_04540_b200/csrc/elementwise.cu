@@ -145,19 +145,20 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
   float nf = 0.0f;
+  const int64_t hi = n4;
   const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
-  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
-       i0 < n4; i0 += step) {
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; i0 < hi;
+       i0 += step) {
     float4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t j = i0 + (int64_t)u * kThreads;
-      if (j < n4) v[u] = __ldcs(x4 + j);
+      if (j < hi) v[u] = __ldcs(x4 + j);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t j = i0 + (int64_t)u * kThreads;
-      if (j < n4) {
+      if (j < hi) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
         if (Op::kBits && (M == kNearestEven || (M == kStochastic && IDX4))) {
           // the variates' top words from the FMA-pipe hash (the bit-domain
@@ -262,6 +263,8 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
       const double fill = (double)ctas / (double)(waves * slots);
       if (fill > best + 0.02) { best = fill; u = c; }
     }
+    // (a resident grid with equal contiguous shares per CTA, so every SM
+    // finishes together, measured slower: C1 5187 -> 4945 GB/s)
     const int64_t want = (work + (int64_t)kThreads * u - 1) / ((int64_t)kThreads * u);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
     if (u == 5)

@@ -135,6 +135,50 @@ __device__ __forceinline__ bool bf16raw_path_ok(const GemmScan& s, int64_t K) {
 }
 
 // ---------------------------------------------------------------------------
+// k_qgemm_bits: any float formats whose mantissa fits the bit-domain form
+// (man <= 22), NearestEven or Stochastic, when the pre-scan proves every
+// product and partial sum is zero or inside both formats' normal ranges
+// (bits_path_ok).  Then each Q is quant_float_bits -- an integer add of the
+// rounding increment (RNE: half a step; stochastic: the reference variate's
+// top bits, complemented for x >= 0) and a mask of the dropped bits -- with no
+// clamp, no underflow grid and no branches; the variates of a thread's 4
+// consecutive outputs share hash work (variate24_x4_top).  Same 64x64 tile
+// and k order as k_qgemm_general.
+//   Proof: nonzero operands normal; every product Qm(fl32(a b)) is a multiple
+//   of G = 2^(ea_min + eb_min - man_m), and sums of multiples of G stay
+//   multiples of G under fp32 adds and either rounding, so every nonzero
+//   value is >= G >= 2^max(min_exp_m, min_exp_a); and |value| stays below
+//   K |a|max |b|max (1 + 2^-man)^(K+1) < 2^min(max_exp_m, max_exp_a).
+__device__ __forceinline__ bool bits_path_ok(const GemmScan& s, int64_t K,
+                                             const FloatParams& qm, const FloatParams& qa) {
+  if (s.nonfinite || !qm.bits_ok || !qa.bits_ok) return false;
+  if (s.a_min_nz_exp_field == 0 || s.b_min_nz_exp_field == 0)
+    return true;  // A or B is all zeros: every product and sum is +-0
+  const int fa = 255 - (int)s.a_min_nz_exp_field, fb = 255 - (int)s.b_min_nz_exp_field;
+  if (fa == 0 || fb == 0) return false;  // a subnormal operand
+  const int ea_min = fa - 127, eb_min = fb - 127;
+  const int ea_max = (int)s.a_max_exp_field - 127;
+  const int eb_max = (int)s.b_max_exp_field - 127;
+  if (ea_min + eb_min - qm.man < max(qm.min_exp, qa.min_exp)) return false;
+  const int man = min(qm.man, qa.man);
+  const double lg = log2((double)K) + (ea_max + 1) + (eb_max + 1) +
+                    (double)(K + 1) * log2(1.0 + ldexp(1.0, -man)) + 1.0;
+  return lg < (double)min(qm.max_exp, qa.max_exp);
+}
+
+// which kernel of a quant_gemm launch computes the product (each kernel
+// evaluates this on the device from the pre-scan and exits unless it is the
+// one): flags bit 0: float(8,7) RNE (the bf16 kernels may run), bit 1: the
+// bits kernel may run.  0: exact bf16, 1: raw bf16, 2: bits, 3: general.
+__device__ __forceinline__ int gemm_kernel_choice(const GemmScan& s, int64_t K, int flags,
+                                                  const FloatParams& qm, const FloatParams& qa) {
+  if ((flags & 1) && bf16_path_ok(s, K)) return 0;
+  if ((flags & 1) && bf16raw_path_ok(s, K)) return 1;
+  if ((flags & 2) && bits_path_ok(s, K, qm, qa)) return 2;
+  return 3;
+}
+
+// ---------------------------------------------------------------------------
 // k_qgemm_bf16: 128x128 CTA tile, 128 threads, 8x16 outputs per thread held
 // as 64 bf16x2 accumulators; K staged 16 at a time into double-buffered
 // shared memory as bf16 (A transposed so a thread's 8 rows are one 16-byte
@@ -347,21 +391,21 @@ __device__ __forceinline__ float qf(float x, const FloatParams& p, uint32_t v) {
   return quant_float<M>(x, p, v);
 }
 
-template <int M_, bool ALWAYS>
+template <int M_>
 __global__ void __launch_bounds__(kGT)
     k_qgemm_general(const float* __restrict__ A, const float* __restrict__ B,
                     float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                     int64_t row_base, FloatParams qm, FloatParams qa,
                     uint64_t seed, uint64_t call,
-                    const GemmScan* __restrict__ scan,
+                    const GemmScan* __restrict__ scan, int flags,
                     uint32_t* __restrict__ status) {
   if (scan->nonfinite) {  // non-finite operands are rejected like quantize
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
       atomicOr(status, kStatusNonFinite);
     return;
   }
-  if (!ALWAYS && (bf16_path_ok(*scan, K) || bf16raw_path_ok(*scan, K)))
-    return;  // a bf16 kernel did it
+  if (gemm_kernel_choice(*scan, K, flags, qm, qa) != 3)
+    return;  // another kernel of the launch did it
   __shared__ float As[kGK][kGM];
   __shared__ float Bs[kGK][kGN];
   __shared__ uint64_t keys[kGK][2];
@@ -442,6 +486,90 @@ __global__ void __launch_bounds__(kGT)
   }
 }
 
+template <int M_, bool X4>
+__global__ void __launch_bounds__(kGT)
+    k_qgemm_bits(const float* __restrict__ A, const float* __restrict__ B,
+                 float* __restrict__ C, int64_t M, int64_t N, int64_t K,
+                 int64_t row_base, FloatParams qm, FloatParams qa,
+                 uint64_t seed, uint64_t call, const GemmScan* __restrict__ scan,
+                 int flags, RngMul rm) {
+  if (gemm_kernel_choice(*scan, K, flags, qm, qa) != 2) return;
+  __shared__ __align__(16) float As[kGK][kGM];
+  __shared__ __align__(16) float Bs[kGK][kGN];
+  __shared__ uint64_t keys[kGK][2];
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * kGM, n0 = (int64_t)blockIdx.x * kGN;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  uint64_t idx[4];  // flat output index of column tx*4 of row i (the variates')
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    idx[i] = (uint64_t)(row_base + m0 + ty * 4 + i) * (uint64_t)N + (uint64_t)(n0 + tx * 4);
+  // (the ALU-leaning variate24_x4, not the FMA-leaning _top form: the
+  // GEMM's own FMUL/FADD and the bits' adds already load the FMA pipe)
+  auto q = [&](float v, const FloatParams& p, uint32_t var) {
+    return M_ == kStochastic ? quant_float_bits<kStochastic>(v, p, var)
+                             : quant_float_bits<kNearestEven>(v, p, 0u);
+  };
+  auto vars = [&](uint64_t key, uint64_t id, uint32_t (&var)[4]) {
+    if (M_ != kStochastic) return;
+    if (X4) {
+      variate24_x4(key, id, rm.m32, var);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) var[j] = variate24(key, id + (uint64_t)j);
+    }
+  };
+  for (int64_t k0 = 0; k0 < K; k0 += kGK) {
+    for (int e = t; e < kGM * kGK; e += kGT) {
+      const int r = e / kGK, c = e % kGK;  // A tile, coalesced along k
+      const int64_t gr = m0 + r, gc = k0 + c;
+      As[c][r] = (gr < M && gc < K) ? A[gr * K + gc] : 0.0f;
+      const int kr = e / kGN, nc = e % kGN;  // B tile, coalesced along n
+      const int64_t gk = k0 + kr, gn = n0 + nc;
+      Bs[kr][nc] = (gk < K && gn < N) ? B[gk * N + gn] : 0.0f;
+    }
+    if (M_ == kStochastic && t < 2 * kGK) {
+      const int kk = t >> 1, op = t & 1;
+      keys[kk][op] = stream_key(seed, call + 2 * (uint64_t)(k0 + kk) + op);
+    }
+    __syncthreads();
+    const int kk_end = (int)min((int64_t)kGK, K - k0);
+    for (int kk = 0; kk < kk_end; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+      uint64_t km = 0, ka = 0;
+      if (M_ == kStochastic) { km = keys[kk][0]; ka = keys[kk][1]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t vm[4] = {0u, 0u, 0u, 0u}, va[4] = {0u, 0u, 0u, 0u};
+        vars(km, idx[i], vm);
+        vars(ka, idx[i], va);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] = q(fadd(acc[i][j], q(fmul(a[i], b[j]), qm, vm[j])), qa, va[j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + ty * 4 + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t col = n0 + tx * 4 + j;
+      if (col < N) C[row * N + col] = acc[i][j];
+    }
+  }
+}
+
 bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
@@ -449,16 +577,23 @@ bool aligned16(const void* p) {
 template <int M_>
 void launch_general(const float* A, const float* B, float* C, int64_t M,
                     int64_t N, int64_t K, int64_t row_base,
-                    const FloatParams& qm, const FloatParams& qa, bool always,
+                    const FloatParams& qm, const FloatParams& qa, int flags,
                     uint64_t seed, uint64_t call, GemmScan* scan,
                     uint32_t* status, cudaStream_t s) {
   dim3 grid((unsigned)((N + kGN - 1) / kGN), (unsigned)((M + kGM - 1) / kGM));
-  if (always)
-    k_qgemm_general<M_, true><<<grid, kGT, 0, s>>>(A, B, C, M, N, K, row_base, qm, qa,
-                                                   seed, call, scan, status);
-  else
-    k_qgemm_general<M_, false><<<grid, kGT, 0, s>>>(A, B, C, M, N, K, row_base, qm, qa,
-                                                    seed, call, scan, status);
+  if constexpr (M_ == kNearestEven || M_ == kStochastic) {
+    if (flags & 2) {  // the bit-domain kernel (it checks its proof itself)
+      if (N % 4 == 0)
+        k_qgemm_bits<M_, true><<<grid, kGT, 0, s>>>(A, B, C, M, N, K, row_base, qm, qa, seed,
+                                                    call, scan, flags, rng_mul());
+      else
+        k_qgemm_bits<M_, false><<<grid, kGT, 0, s>>>(A, B, C, M, N, K, row_base, qm, qa, seed,
+                                                     call, scan, flags, rng_mul());
+      note_launch();
+    }
+  }
+  k_qgemm_general<M_><<<grid, kGT, 0, s>>>(A, B, C, M, N, K, row_base, qm, qa, seed, call,
+                                           scan, flags, status);
   note_launch();
 }
 
@@ -702,11 +837,14 @@ cudaError_t launch_quant_gemm(const float* A, const float* B, float* C,
     }
     note_launch(2);
   }
+  const bool try_bits = (mode == kNearestEven || mode == kStochastic) && qm.bits_ok &&
+                        qa.bits_ok;
+  const int flags = (try_bf16 ? 1 : 0) | (try_bits ? 2 : 0);
   switch (mode) {
-    case kStochastic: launch_general<kStochastic>(A, B, C, M, N, K, row_base, qm, qa, !try_bf16, seed, call, scan, status, s); break;
-    case kNearestAway: launch_general<kNearestAway>(A, B, C, M, N, K, row_base, qm, qa, !try_bf16, seed, call, scan, status, s); break;
-    case kNearestZero: launch_general<kNearestZero>(A, B, C, M, N, K, row_base, qm, qa, !try_bf16, seed, call, scan, status, s); break;
-    default: launch_general<kNearestEven>(A, B, C, M, N, K, row_base, qm, qa, !try_bf16, seed, call, scan, status, s); break;
+    case kStochastic: launch_general<kStochastic>(A, B, C, M, N, K, row_base, qm, qa, flags, seed, call, scan, status, s); break;
+    case kNearestAway: launch_general<kNearestAway>(A, B, C, M, N, K, row_base, qm, qa, flags, seed, call, scan, status, s); break;
+    case kNearestZero: launch_general<kNearestZero>(A, B, C, M, N, K, row_base, qm, qa, flags, seed, call, scan, status, s); break;
+    default: launch_general<kNearestEven>(A, B, C, M, N, K, row_base, qm, qa, flags, seed, call, scan, status, s); break;
   }
   return cudaGetLastError();
 }

@@ -98,6 +98,28 @@ def test_quant_gemm_raw_guards(q, oracle, case):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want)), case
 
 
+@pytest.mark.parametrize("fm,fa,K", [((8, 7), (8, 7), 300), ((8, 10), (8, 3), 200),
+                                     ((5, 10), (5, 10), 64), ((5, 2), (5, 2), 12),
+                                     ((4, 3), (6, 5), 8)])
+@pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
+@pytest.mark.parametrize("N", [64, 30])
+def test_quant_gemm_bit_domain_kernel(q, oracle, fm, fa, K, mode, N):
+    # operands in [0.5, 2) with random signs keep every product and sum
+    # inside both formats' normal ranges for these K, so the pre-scan selects
+    # k_qgemm_bits (bit-domain Q after every op); N = 30 takes its scalar-
+    # variate form (flat indices of a thread's 4 columns not 4-aligned)
+    rng = np.random.default_rng(fm[0] * 100 + fa[1] * 10 + mode + N)
+    M = 70
+    a = (rng.uniform(0.5, 2.0, (M, K)) * rng.choice([-1, 1], (M, K))).astype(np.float32)
+    b = (rng.uniform(0.5, 2.0, (K, N)) * rng.choice([-1, 1], (K, N))).astype(np.float32)
+    st, want = oracle.quant_gemm(a, b, float_fmt(*fm), float_fmt(*fa), mode,
+                                 seed=1234, call=6, row_base=3)
+    assert st == 0
+    got = q.quant_gemm(dev(a), dev(b), q.FloatFormat(*fm), q.FloatFormat(*fa),
+                       q.RoundingMode(mode), 1234, 6, row_base=3)
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want)), (fm, fa, mode, N)
+
+
 def test_quant_gemm_underflow_guard(q, oracle):
     # bf16-exact operands whose products fall below 2^-126: the device-side
     # pre-scan must route to the general kernel (two-point underflow grid)
