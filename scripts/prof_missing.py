@@ -4,6 +4,7 @@
 
 general : k_qgemm_general (per-op GEMM float(5,2) stochastic, 2048^3, raw fp32 inputs)
 raw     : k_qgemm_bf16<raw> (per-op GEMM float(8,7) nearest, 4096^3, raw fp32 inputs)
+bits    : k_qgemm_bits (per-op GEMM float(8,7) stochastic, 2048^3, raw fp32 inputs)
 seg     : k_seg_reduce + k_seg_apply (block(8) whole tensor, 2^28)
 col     : k_col_reduce + k_col_apply (block(8) dim 1 on [2^22, 64])
 group   : k_group_elementwise / k_group_block_rows (ResNet-50 weights, grouped)
@@ -31,6 +32,13 @@ if what == "general":
     c = torch.empty((n, n), device="cuda")
     for _ in range(reps):
         q.quant_gemm(a, b, q.FloatFormat(5, 2), q.FloatFormat(5, 2), S, 3, out=c, sync=False)
+elif what == "bits":
+    n = 2048
+    a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
+    b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
+    c = torch.empty((n, n), device="cuda")
+    for _ in range(reps):
+        q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7), S, 3, out=c, sync=False)
 elif what == "raw":
     n = 4096
     a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
