@@ -48,13 +48,13 @@ constexpr int kT = 256;  // threads per CTA
 // and CTAs per SM.  Measured on B200 against (16 float4, 2 CTAs/SM), (8, 3),
 // (4, 6), (4, 8), (6, 4) on the ResNet-50 activation rows (scripts/
 // time_act_plans.py): more resident CTAs hide the rendezvous and load
-// latencies until the register cap spills; [256, 802816] nearest 4607 ->
-// 4673 GB/s, stochastic 5801 -> 5967.  Also measured and slower: a
-// shared-memory variant double-buffering chunks with cp.async, the next
-// chunk's loads issued before the rendezvous, 3 CTAs/SM (3867 / 4710); a
-// register double-buffered one, 2 CTAs/SM (3518 / 4596), and with 4 float4
-// per thread at 4 CTAs/SM (3567 / 4511); 128-thread CTAs x 8
-// per SM (3772 / 4425); the L2 prefetch two rounds ahead (4425 / 5740).
+// latencies until the register cap spills; [256, 802816] stochastic 4607 ->
+// 4673 GB/s, nearest 5801 -> 5967.  Also measured and slower (stochastic /
+// nearest): a shared-memory variant double-buffering chunks with cp.async,
+// the next chunk's loads issued before the rendezvous, 3 CTAs/SM (3867 /
+// 4710); a register double-buffered one, 2 CTAs/SM (3518 / 4596), and with
+// 4 float4 per thread at 4 CTAs/SM (3567 / 4511); 128-thread CTAs x 8 per SM
+// (3772 / 4425); the L2 prefetch two rounds ahead (4425 / 5740).
 constexpr int kV = 8;
 constexpr int kB = 4;
 
