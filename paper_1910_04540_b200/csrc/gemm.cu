@@ -509,21 +509,23 @@ __global__ void __launch_bounds__(kGT)
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     idx[i] = (uint64_t)(row_base + m0 + ty * 4 + i) * (uint64_t)N + (uint64_t)(n0 + tx * 4);
-  // (the ALU-leaning variate24_x4, not the FMA-leaning _top form: the
-  // GEMM's own FMUL/FADD and the bits' adds already load the FMA pipe)
-  auto q = [&](float v, const FloatParams& p, uint32_t var) {
-    return M_ == kStochastic ? quant_float_bits<kStochastic>(v, p, var)
-                             : quant_float_bits<kNearestEven>(v, p, 0u);
+  // the ALU-leaning variate24_x4 for both ops (the FMA-leaning _top form for
+  // both: 953 GFLOP/s on c4s, for the multiply's only: 1064, neither: 1109)
+  auto q = [&](float v, const FloatParams& p, uint32_t var, bool top) {
+    if (M_ != kStochastic) return quant_float_bits<kNearestEven>(v, p, 0u);
+    return top ? quant_float_bits_top(v, p, var, rm.one) : quant_float_bits<kStochastic>(v, p, var);
   };
-  auto vars = [&](uint64_t key, uint64_t id, uint32_t (&var)[4]) {
+  auto vars = [&](uint64_t key, uint64_t id, uint32_t (&var)[4], bool top) {
     if (M_ != kStochastic) return;
     if (X4) {
-      variate24_x4(key, id, rm.m32, var);
+      if (top) variate24_x4_top(key, id, rm, var);
+      else variate24_x4(key, id, rm.m32, var);
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) var[j] = variate24(key, id + (uint64_t)j);
+      for (int j = 0; j < 4; ++j) var[j] = variate24(key, id + (uint64_t)j) << (top ? 8 : 0);
     }
   };
+  constexpr bool kTopM = false;
   for (int64_t k0 = 0; k0 < K; k0 += kGK) {
     for (int e = t; e < kGM * kGK; e += kGT) {
       const int r = e / kGK, c = e % kGK;  // A tile, coalesced along k
@@ -549,11 +551,11 @@ __global__ void __launch_bounds__(kGT)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t vm[4] = {0u, 0u, 0u, 0u}, va[4] = {0u, 0u, 0u, 0u};
-        vars(km, idx[i], vm);
-        vars(ka, idx[i], va);
+        vars(km, idx[i], vm, kTopM);
+        vars(ka, idx[i], va, false);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          acc[i][j] = q(fadd(acc[i][j], q(fmul(a[i], b[j]), qm, vm[j])), qa, va[j]);
+          acc[i][j] = q(fadd(acc[i][j], q(fmul(a[i], b[j]), qm, vm[j], kTopM)), qa, va[j], false);
       }
     }
     __syncthreads();
