@@ -54,7 +54,10 @@ constexpr int kT = 256;  // threads per CTA
 // the next chunk's loads issued before the rendezvous, 3 CTAs/SM (3867 /
 // 4710); a register double-buffered one, 2 CTAs/SM (3518 / 4596), and with
 // 4 float4 per thread at 4 CTAs/SM (3567 / 4511); 128-thread CTAs x 8 per SM
-// (3772 / 4425); the L2 prefetch two rounds ahead (4425 / 5740).
+// (3772 / 4425); the L2 prefetch two rounds ahead (4425 / 5740); staging the
+// next chunk in shared memory by cp.async and arriving it BEFORE quantizing
+// the current one, so a row's arrivals never wait on a CTA's stochastic
+// quantize pass (4084 / 5465).
 constexpr int kV = 8;
 constexpr int kB = 4;
 
