@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/lpq.h"
@@ -30,8 +31,7 @@ constexpr int kMaxGroup = 64;
 constexpr int kT = 256;
 constexpr int kEwU = 8;                        // float4 per thread (elementwise)
 constexpr int64_t kTile = (int64_t)kT * kEwU * 4;  // elements per CTA
-constexpr int kRowV = 32;                      // floats per thread (block rows)
-constexpr int64_t kMaxRow = (int64_t)kT * kRowV;   // 8192
+constexpr int64_t kMaxRow = 8192;              // longest grouped block row (floats)
 
 struct Entry {
   const float* x;
@@ -135,50 +135,72 @@ __global__ void __launch_bounds__(kT)
     atomicOr(status, kStatusNonFinite);
 }
 
-// block format along dim 0: one CTA per row (row length <= kMaxRow floats)
+// Block format along dim 0 (rows of <= kMaxRow floats): one WARP per row,
+// 8 rows per CTA.  Pass 1 streams the row (float4 when the rows are 16-byte
+// aligned) and reduces max|x| over the warp; pass 2 re-reads it -- 36 KB at
+// most per CTA, an L1 / L2 hit, so HBM sees one read and one write -- and
+// quantizes with the float4-shared variates.  (One 256-thread CTA per row
+// holding 32 floats per thread in registers issued all 32 predicated slots
+// for the 64-576-float rows of the ResNet-50 weights: 786 GB/s,
+// profiles/r02_group_block_rows_r50w.raw.csv.)
+constexpr int kRowsPerCta = kT / 32;
+
 template <int M>
 __global__ void __launch_bounds__(kT)
     k_group_block_rows(const __grid_constant__ Table t, int wl,
                        uint32_t* __restrict__ status) {
-  __shared__ uint32_t red[kT / 32];
-  __shared__ uint32_t row_max;
   const Entry& e = t.e[find_entry(t, blockIdx.x)];
-  const int64_t r = blockIdx.x - e.first;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = (blockIdx.x - e.first) * kRowsPerCta + warp;
+  const int64_t rows = e.n / e.len;
+  if (r >= rows) return;  // (no CTA-wide barriers below)
   const float* __restrict__ x = e.x + r * e.len;
   float* __restrict__ y = e.y + r * e.len;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float v[kRowV];
+  const uint64_t rb = e.base + (uint64_t)(r * e.len);
+  const bool vec = (e.len & 3) == 0 &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
+  const int64_t len4 = e.len >> 2;
   float mf = 0.0f, nf = 0.0f;
-#pragma unroll
-  for (int k = 0; k < kRowV; ++k) {
-    const int64_t j = threadIdx.x + (int64_t)k * kT;
-    v[k] = j < e.len ? __ldcs(x + j) : 0.0f;
-    mf = fmaxf(mf, fabsf(v[k]));
-    nf = __fmaf_rn(v[k], 0.0f, nf);
+  if (vec) {
+    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t j = lane; j < len4; j += 32) {
+      const float4 v = __ldg(x4 + j);
+      absmax_nf(v, mf, nf);
+    }
+  } else {
+    for (int64_t j = lane; j < e.len; j += 32) {
+      const float v = __ldg(x + j);
+      mf = fmaxf(mf, fabsf(v));
+      nf = __fmaf_rn(v, 0.0f, nf);
+    }
   }
-  uint32_t m = __reduce_max_sync(kFull, f2u(mf));
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t tt = lane < kT / 32 ? red[lane] : 0u;
-    tt = __reduce_max_sync(kFull, tt);
-    if (lane == 0) row_max = tt;
-  }
-  __syncthreads();
-  const BlockScale sc = make_block_scale(row_max, wl);
+  const uint32_t m = __reduce_max_sync(kFull, f2u(mf));
+  const BlockScale sc = make_block_scale(m, wl);
   const float kmin = -(float)(1 << (wl - 1));
   const float kmax = (float)((1 << (wl - 1)) - 1);
-  const uint64_t rb = e.base + (uint64_t)(r * e.len);
   const RngMul rm = rng_mul();
-#pragma unroll
-  for (int k = 0; k < kRowV; ++k) {
-    const int64_t j = threadIdx.x + (int64_t)k * kT;
-    if (j < e.len)
-      y[j] = two_factor(sc) ? qb<M, true>(v[k], sc, kmin, kmax, e.key ^ (rb + j), rm)
-                            : qb<M, false>(v[k], sc, kmin, kmax, e.key ^ (rb + j), rm);
-  }
-  uint32_t bad = (sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u);
-  bad = __reduce_or_sync(kFull, bad);
+  auto run = [&](auto two_t) {
+    constexpr bool TWO = decltype(two_t)::value;
+    if (vec) {
+      const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x);
+      float4* __restrict__ y4 = reinterpret_cast<float4*>(y);
+      if ((rb & 3u) == 0) {
+        for (int64_t j = lane; j < len4; j += 32)
+          __stcs(y4 + j, qb4<M, TWO, true>(__ldcs(x4 + j), sc, kmin, kmax, e.key,
+                                           rb + 4 * j, rm));
+      } else {
+        for (int64_t j = lane; j < len4; j += 32)
+          __stcs(y4 + j, qb4<M, TWO, false>(__ldcs(x4 + j), sc, kmin, kmax, e.key,
+                                            rb + 4 * j, rm));
+      }
+    } else {
+      for (int64_t j = lane; j < e.len; j += 32)
+        y[j] = qb<M, TWO>(__ldcs(x + j), sc, kmin, kmax, e.key ^ (rb + j), rm);
+    }
+  };
+  if (two_factor(sc)) run(std::true_type{});
+  else run(std::false_type{});
+  const uint32_t bad = __reduce_or_sync(kFull, (sc.bad ? 2u : 0u) | (nf != nf ? 1u : 0u));
   if (lane == 0 && bad) atomicOr(status, bad);
 }
 
@@ -267,7 +289,8 @@ extern "C" lpq_status lpq_quantize_grouped(const lpq_tensor_desc* tensors,
     e.base = d.index_base;
     e.key = stream_key(seed, d.call);
     e.first = t.ctas;
-    t.ctas += f->kind == LPQ_BLOCK ? g.extent : (n + kTile - 1) / kTile;
+    t.ctas += f->kind == LPQ_BLOCK ? (g.extent + kRowsPerCta - 1) / kRowsPerCta
+                                   : (n + kTile - 1) / kTile;
   }
   return flush();
 }
