@@ -636,7 +636,13 @@ bool block_cluster_ok(const BlockGeom& g, const float* x, const float* y) {
 BlockPlan block_plan(const BlockGeom& g, const float* x, const float* y) {
   const bool rows = g.outer == 1 && g.stride % 4 == 0 && aligned16(x) && aligned16(y);
   if (rows && g.stride <= 32768 && g.stride >= 4) return BlockPlan::kRowsInRegisters;
-  // longer rows of up to ~1M floats: chunk rendezvous (one HBM pass, every
+  // rows of 32K-75K floats: 2-CTA clusters ([256, 50176]: 5169 GB/s nearest
+  // vs 3847 on the chunk plan, whose 7 chunks per row leave a fourth round
+  // of 16 CTAs; at 100352 the two are even), when they fill the GPU
+  if (block_cluster_ok(g, x, y) && g.stride <= 75000 &&
+      g.extent * cluster_size_for(g.stride) >= 2 * (int64_t)device_info().sm_count)
+    return BlockPlan::kRowsCluster;
+  // longer rows of up to ~2.4M floats: chunk rendezvous (one HBM pass, every
   // SM busy; needs the workspace -- quantize_device takes the cluster plan
   // when the caller supplied none)
   if (rows && block_chunks_ok(g.stride, g.extent)) return BlockPlan::kRowsChunked;

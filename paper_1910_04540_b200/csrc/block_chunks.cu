@@ -57,7 +57,10 @@ constexpr int kT = 256;  // threads per CTA
 // (3772 / 4425); the L2 prefetch two rounds ahead (4425 / 5740); staging the
 // next chunk in shared memory by cp.async and arriving it BEFORE quantizing
 // the current one, so a row's arrivals never wait on a CTA's stochastic
-// quantize pass (4084 / 5465).
+// quantize pass (4084 / 5465); up to twice as many smaller chunks per row
+// when that fills the last round of the grid better ([256, 50176] 3847 ->
+// 4169 nearest, but [256, 401408] 5873 -> 5462 and [256, 200704] 5478 ->
+// 4960: the rendezvous cost per chunk outweighs the waves).
 constexpr int kV = 8;
 constexpr int kB = 4;
 

@@ -11,7 +11,7 @@ import paper_1910_04540_b200 as q
 from paper_1910_04540_b200 import _lib
 
 shapes = [(256, 64, 112, 112), (256, 256, 56, 56), (256, 128, 56, 56), (256, 512, 28, 28),
-          (256, 1024, 14, 14), (256, 2048, 7, 7), (256, 64, 56, 56)]
+          (256, 1024, 14, 14), (256, 2048, 7, 7), (256, 64, 56, 56), (256, 256, 14, 14)]
 status = torch.zeros(1, dtype=torch.int32, device="cuda")
 wsb = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
 stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -137,11 +137,12 @@ BLOCK_CASES = [
     ((300, 4096), 0),       # rows in registers, 1024x4
     ((64, 100), 0),         # rows, 128 threads
     ((7, 20000), 0),        # rows, 1024 x 8 float4
-    ((5, 40000), 0),        # few long rows -> two-pass segments
-    ((300, 40000), 0),      # chunk rendezvous, 3 chunks per row
+    ((5, 40000), 0),        # few rows of 40K: chunk rendezvous (3 chunks per row)
+    ((300, 40000), 0),      # many rows of 40K: 2-CTA clusters (DSMEM max exchange)
     ((80, 200000), 0),      # chunk rendezvous, 13 chunks per row (ragged last)
     ((40, 802816), 0),      # ResNet-50 conv1 per-sample block, 49 chunks per row
-    ((1, 300, 40000), 1),   # chunk rendezvous along dim 1 (leading 1)
+    ((1, 300, 40000), 1),   # clusters along dim 1 (leading 1)
+    ((256, 50176), 0),      # ResNet-50 [256, 256, 14, 14] per-sample rows: clusters
     ((2, 65540), 0),        # 5 chunks of 13108 floats (uneven split)
     ((1 << 20,), None),     # whole tensor, one row of 64 chunks
     ((4096, 64), 0),        # short rows: 16 lanes per row
