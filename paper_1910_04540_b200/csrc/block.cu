@@ -523,8 +523,15 @@ cudaError_t launch_block_m(const float* x, float* y, const BlockGeom& g,
     launch_rows<M>(x, y, g.stride, g.extent, base, key, wl, status, s);
     return cudaGetLastError();
   }
-  if (plan == BlockPlan::kRowsChunked)
-    return launch_block_chunks(x, y, g.stride, g.extent, base, key, wl, M, ws, status, s);
+  if (plan == BlockPlan::kRowsChunked) {
+    const cudaError_t e = launch_block_chunks(x, y, g.stride, g.extent, base, key, wl, M, ws,
+                                              status, s);
+    if (e != cudaErrorCooperativeLaunchTooLarge) return e;
+    // fewer SMs than the occupancy query saw (MPS / green contexts): the
+    // two-pass segment plan (its maxima fit the chunk plan's workspace)
+    cudaGetLastError();
+    plan = BlockPlan::kTwoPassSegments;
+  }
   if (plan == BlockPlan::kRowsCluster)
     return launch_block_cluster(x, y, g.stride, g.extent, base, key, wl, M,
                                 status, s);
