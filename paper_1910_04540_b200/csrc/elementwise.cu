@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
           // runs the per-element forms for every lane, instead of diverging
           // into both paths (mixed warps, e.g. log-uniform magnitudes, paid
           // for both): C1 log-uniform stochastic 3492 -> 3806 GB/s, nearest
-          // 5061 -> 5595, at ~1 % on uniform stochastic (the vote)
+          // 5061 -> 5595, at ~1 % on uniform stochastic (the vote; a
+          // full-mask vote for warps wholly inside the tensor, behind a
+          // warp-uniform test, was slower: C1 4662, log-uniform 3612)
           if (__all_sync(__activemask(), op.in_range4(v[u]))) {
             o = op.template bits4<M>(v[u], tt, rm.one);
           } else {
