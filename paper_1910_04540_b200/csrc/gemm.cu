@@ -509,23 +509,23 @@ __global__ void __launch_bounds__(kGT)
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     idx[i] = (uint64_t)(row_base + m0 + ty * 4 + i) * (uint64_t)N + (uint64_t)(n0 + tx * 4);
-  // the ALU-leaning variate24_x4 for both ops (the FMA-leaning _top form for
-  // both: 953 GFLOP/s on c4s, for the multiply's only: 1064, neither: 1109)
-  auto q = [&](float v, const FloatParams& p, uint32_t var, bool top) {
+  // variates as top words from the ALU-leaning hash (its final >> 8 folded
+  // into quant_float_bits_top, whose sign spread and carry add issue on the
+  // FMA pipe): c4s 1109 -> 1130 GFLOP/s.  (The FMA-leaning variate24_x4_top
+  // for both ops: 953, for the multiply's only: 1064.)
+  auto q = [&](float v, const FloatParams& p, uint32_t top) {
     if (M_ != kStochastic) return quant_float_bits<kNearestEven>(v, p, 0u);
-    return top ? quant_float_bits_top(v, p, var, rm.one) : quant_float_bits<kStochastic>(v, p, var);
+    return quant_float_bits_top(v, p, top, rm.one);
   };
-  auto vars = [&](uint64_t key, uint64_t id, uint32_t (&var)[4], bool top) {
+  auto vars = [&](uint64_t key, uint64_t id, uint32_t (&top)[4]) {
     if (M_ != kStochastic) return;
     if (X4) {
-      if (top) variate24_x4_top(key, id, rm, var);
-      else variate24_x4(key, id, rm.m32, var);
+      variate24_x4<true>(key, id, rm.m32, top);
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) var[j] = variate24(key, id + (uint64_t)j) << (top ? 8 : 0);
+      for (int j = 0; j < 4; ++j) top[j] = variate24(key, id + (uint64_t)j) << 8;
     }
   };
-  constexpr bool kTopM = false;
   for (int64_t k0 = 0; k0 < K; k0 += kGK) {
     for (int e = t; e < kGM * kGK; e += kGT) {
       const int r = e / kGK, c = e % kGK;  // A tile, coalesced along k
@@ -551,11 +551,11 @@ __global__ void __launch_bounds__(kGT)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t vm[4] = {0u, 0u, 0u, 0u}, va[4] = {0u, 0u, 0u, 0u};
-        vars(km, idx[i], vm, kTopM);
-        vars(ka, idx[i], va, false);
+        vars(km, idx[i], vm);
+        vars(ka, idx[i], va);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          acc[i][j] = q(fadd(acc[i][j], q(fmul(a[i], b[j]), qm, vm[j], kTopM)), qa, va[j], false);
+          acc[i][j] = q(fadd(acc[i][j], q(fmul(a[i], b[j]), qm, vm[j])), qa, va[j]);
       }
     }
     __syncthreads();

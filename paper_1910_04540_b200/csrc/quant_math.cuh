@@ -263,6 +263,9 @@ LPQ_HD uint32_t mulhi_sep(uint32_t a, uint32_t b) {
 #endif
 }
 
+// TOP = true: out[q] is the variate's top word (variate = top >> 8, the low
+// 8 bits arbitrary) for quant_float_bits_top, which folds the shift
+template <bool TOP = false>
 LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
                          uint32_t out[4]) {  // m32: the generic fallback's
   const uint64_t z0 = key ^ idx;
@@ -270,7 +273,7 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
   const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
   const uint32_t kl = (uint32_t)key & 3u;
   if (wlo > 0xFFFFFFFCu) {  // w + j_q may carry into the high word
-    for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m32);
+    for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m32) << (TOP ? 8 : 0);
     return;
   }
   const uint32_t h1 = whi ^ (whi >> 30);                   // shared
@@ -291,7 +294,7 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
     plo ^= slo;
     phi ^= shi;
     const uint32_t top = mulhi_sep(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
-    out[q] = top >> 8;
+    out[q] = TOP ? top : top >> 8;
   }
 }
 

@@ -105,6 +105,13 @@ void hm_variates24_fma(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
 void hm_variates24_x4(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   for (int64_t i = 0; i < n; i += 4) lpq::variate24_x4(key, base + (uint64_t)i, 32u, out + i);
 }
+// the ALU-leaning float4 form returning top words (variate = top >> 8)
+void hm_variates24_x4_topw(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
+  for (int64_t i = 0; i < n; i += 4) {
+    lpq::variate24_x4<true>(key, base + (uint64_t)i, 32u, out + i);
+    for (int q = 0; q < 4; ++q) out[i + q] >>= 8;
+  }
+}
 // the top-word float4 form (variate = top >> 8)
 void hm_variates24_x4_top(uint64_t key, uint64_t base, int64_t n, uint32_t* out) {
   const lpq::RngMul m = lpq::rng_mul();

@@ -38,6 +38,7 @@ def hm():
     L.hm_variates24_fma.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_x4.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_variates24_x4_top.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
+    L.hm_variates24_x4_topw.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, up]
     L.hm_quant_float_bits_top.argtypes = [fp, up, fp, C.c_int64, C.c_int, C.c_int]
     L.hm_quant_float_bits.argtypes = [fp, up, fp, C.c_int64, C.c_int, C.c_int]
     return L
@@ -107,6 +108,8 @@ def test_float4_variate_form_is_identical(hm):
         assert np.array_equal(a, b), (key, base)
         hm.hm_variates24_x4_top(key, base, n, b)
         assert np.array_equal(a, b), (key, base, "top")
+        hm.hm_variates24_x4_topw(key, base, n, b)
+        assert np.array_equal(a, b), (key, base, "topw")
 
 
 @pytest.mark.parametrize("em", [(5, 2), (4, 3), (2, 1), (7, 12), (3, 0), (8, 22)])
