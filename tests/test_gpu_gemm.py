@@ -207,17 +207,21 @@ def _parallel_rows(fn, rows):
         return list(ex.map(fn, rows))
 
 
+@pytest.mark.parametrize("operands", ["f87", "raw"])
 @pytest.mark.parametrize("mode", [NEAREST_EVEN, STOCHASTIC])
-def test_c4_quant_gemm_4096_sampled_rows(q, oracle, mode):
-    """C4 (4096^3, float(8,7) after every multiply and add): 64 sampled
-    output rows (tile borders included) vs the oracle, rows in parallel host
-    threads.  Nearest-even runs the bf16 path, stochastic the general path."""
+def test_c4_quant_gemm_4096_sampled_rows(q, oracle, mode, operands):
+    """C4 (4096^3, float(8,7) after every multiply and add; bench configs
+    c4 / c4raw / c4s): 64 sampled output rows (tile borders included) vs the
+    oracle, rows in parallel host threads.  Nearest runs the exact-bf16 kernel
+    on float(8,7) operands and the raw-bf16 kernel on raw fp32 ones;
+    stochastic runs the bit-domain kernel."""
     n = 4096
     a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
     b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
-    f87 = q.QuantSpec(q.FloatFormat(8, 7))
-    a = q.quantize_fused_at(a, f87, 0)
-    b = q.quantize_fused_at(b, f87, 0)
+    if operands == "f87":
+        f87 = q.QuantSpec(q.FloatFormat(8, 7))
+        a = q.quantize_fused_at(a, f87, 0)
+        b = q.quantize_fused_at(b, f87, 0)
     c = q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7), q.RoundingMode(mode),
                      0x15EED, 2).cpu().numpy()
     ah, bh = a.cpu().numpy(), b.cpu().numpy()
