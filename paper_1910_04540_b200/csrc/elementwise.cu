@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
           // for both): C1 log-uniform stochastic 3492 -> 3806 GB/s, nearest
           // 5061 -> 5595, at ~1 % on uniform stochastic (the vote; a
           // full-mask vote for warps wholly inside the tensor, behind a
-          // warp-uniform test, was slower: C1 4662, log-uniform 3612)
+          // warp-uniform test, was slower: C1 4662, log-uniform 3612; so
+          // was deferring the per-element float4s to a cold second loop to
+          // keep the hot code contiguous: C1 4568-4809 vs 5005-5011)
           if (__all_sync(__activemask(), op.in_range4(v[u]))) {
             o = op.template bits4<M>(v[u], tt, rm.one);
           } else {
