@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kT, kB)
 }
 
 template <int M, bool IDX4>
-int resident_ctas_t() {
+int per_sm_t() {  // resident CTAs per SM (a property of the kernel and the arch)
   static int per_sm = -1;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
@@ -222,21 +222,21 @@ int resident_ctas_t() {
       b = 1;
     per_sm = std::max(1, b);
   }
-  return per_sm * device_info().sm_count;
+  return per_sm;
 }
 
-// the least resident count over the instantiations: the grid of every mode
-// (and the progress test in block_chunks_ok)
+// the least resident count over the instantiations on the CURRENT device:
+// the grid of every mode (and the progress test in block_chunks_ok)
 int resident_ctas() {
-  static const int r = std::min({resident_ctas_t<kStochastic, true>(),
-                                  resident_ctas_t<kStochastic, false>(),
-                                  resident_ctas_t<kNearestEven, true>(),
-                                  resident_ctas_t<kNearestEven, false>(),
-                                  resident_ctas_t<kNearestAway, true>(),
-                                  resident_ctas_t<kNearestAway, false>(),
-                                  resident_ctas_t<kNearestZero, true>(),
-                                  resident_ctas_t<kNearestZero, false>()});
-  return r;
+  static const int per_sm = std::min({per_sm_t<kStochastic, true>(),
+                                      per_sm_t<kStochastic, false>(),
+                                      per_sm_t<kNearestEven, true>(),
+                                      per_sm_t<kNearestEven, false>(),
+                                      per_sm_t<kNearestAway, true>(),
+                                      per_sm_t<kNearestAway, false>(),
+                                      per_sm_t<kNearestZero, true>(),
+                                      per_sm_t<kNearestZero, false>()});
+  return per_sm * device_info().sm_count;
 }
 
 // chunk geometry of a row of L floats: cpr chunks of S4 float4 each
