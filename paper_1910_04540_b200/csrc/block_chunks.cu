@@ -60,7 +60,10 @@ constexpr int kT = 256;  // threads per CTA
 // quantize pass (4084 / 5465); up to twice as many smaller chunks per row
 // when that fills the last round of the grid better ([256, 50176] 3847 ->
 // 4169 nearest, but [256, 401408] 5873 -> 5462 and [256, 200704] 5478 ->
-// 4960: the rendezvous cost per chunk outweighs the waves).
+// 4960: the rendezvous cost per chunk outweighs the waves); hashing a
+// stochastic chunk's variates into shared memory while the row's other
+// chunks arrive (stochastic 4547 -> 4463: the kernel is issue-bound, not
+// latency-bound, under stochastic rounding).
 constexpr int kV = 8;
 constexpr int kB = 4;
 
