@@ -83,3 +83,71 @@ def test_random_formats_shapes_modes(chunk):
             continue
         got = q.quantize_fused_at(xd, spec, call, index_base=base).cpu().numpy()
         assert np.array_equal(bits(got), bits(want)), (seed, repr(fmt), mode, x.shape, base)
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1910_04540_b200 as q
+    return q
+
+
+# ---- long block rows: the chunk-rendezvous and cluster plans --------------------
+def _block_rows_case(seed):
+    rng = np.random.default_rng(10_000 + seed)
+    L = int(rng.integers(8193, 300_000)) * 4 if rng.random() < 0.8 else \
+        int(rng.integers(32769, 1_200_000))          # some rows not a multiple of 4
+    rows = int(rng.integers(1, max(2, 24_000_000 // L)))
+    wl = int(rng.integers(2, 25))
+    mode = int(rng.integers(0, 4))
+    base = int(rng.choice([0, int(rng.integers(1, 2 ** 20))]))
+    return L, rows, wl, mode, base
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_long_block_rows(q, oracle, seed):
+    L, rows, wl, mode, base = _block_rows_case(seed)
+    rng = np.random.default_rng(seed)
+    x = q.random_uniform((rows, L), seed, 0, -1.0, 1.0)
+    scale = torch.from_numpy((2.0 ** rng.integers(-40, 40, (rows, 1))).astype(np.float32)).cuda()
+    x = x * scale
+    x[rows // 2, (seed * 7919) % L] = 0.0
+    spec = q.QuantSpec(q.BlockFloatFormat(wl, 0), q.RoundingMode(mode), seed)
+    y = q.quantize_fused_at(x, spec, 5, index_base=base)
+    for r in sorted({0, rows // 2, rows - 1}):
+        xr = x[r:r + 1].cpu().numpy()
+        st, want = oracle.quantize(xr, block_fmt(wl, 0), mode, seed=seed, call=5,
+                                   index_base=base + r * L)
+        assert st == 0
+        assert np.array_equal(bits(y[r:r + 1].cpu().numpy()), bits(want)), (seed, L, rows, wl, mode, r)
+
+
+# ---- the per-op GEMM: every kernel of the launch -----------------------------------
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_quant_gemm(q, oracle, seed):
+    rng = np.random.default_rng(20_000 + seed)
+    M, N, K = (int(rng.integers(1, 70)) for _ in range(3))
+    if rng.random() < 0.4:
+        fm = fa = (8, 7)
+    else:
+        fm = (int(rng.integers(2, 9)), int(rng.integers(0, 24)))
+        fa = (int(rng.integers(2, 9)), int(rng.integers(0, 24)))
+    mode = int(rng.integers(0, 4))
+    lo = float(2.0 ** rng.integers(-8, 1))
+    a = (rng.uniform(lo, 2 * lo, (M, K)) * rng.choice([-1, 1], (M, K))).astype(np.float32)
+    b = (rng.uniform(0.5, 1.5, (K, N)) * rng.choice([-1, 1], (K, N))).astype(np.float32)
+    if rng.random() < 0.3:  # float(8,7)-exact operands (the exact-bf16 kernel's)
+        _, a = oracle.quantize(a, float_fmt(8, 7), 1)
+        _, b = oracle.quantize(b, float_fmt(8, 7), 1)
+    if rng.random() < 0.2:
+        a.reshape(-1)[:: 5] = 0.0
+    got = q.quant_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                       q.FloatFormat(*fm), q.FloatFormat(*fa), q.RoundingMode(mode), seed, 3,
+                       row_base=_row_base_of(seed))
+    st, want = oracle.quant_gemm(a, b, float_fmt(*fm), float_fmt(*fa), mode,
+                                 seed=seed, call=3, row_base=_row_base_of(seed))
+    assert st == 0
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want)), (seed, M, N, K, fm, fa, mode)
+
+
+def _row_base_of(seed):
+    return (seed * 37) % 100
