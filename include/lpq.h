@@ -89,7 +89,12 @@ const char* lpq_status_string(lpq_status s);
 /* validate(fmt): proj/include/lpsim/formats.hpp:82-112 */
 lpq_status lpq_validate_format(const lpq_format* f);
 /* Device workspace the device entry points need for this (format, shape):
- * the per-block maxima of two-pass block formats.  0 for float/fixed. */
+ * block formats -- the per-block maxima of the two-pass plans, or the row
+ * maxima and arrival counters of the single-pass chunk plan for rows of
+ * 32K+ floats (whichever is larger; the device call zeroes what it uses).
+ * 0 for float/fixed.  A block call given no workspace takes a
+ * workspace-free plan where one exists (rows of 32K..1M floats: thread-block
+ * clusters) and returns LPQ_ERR_WORKSPACE otherwise. */
 size_t lpq_workspace_size(const lpq_format* f, const int64_t* shape, int rank);
 /* Number of kernel launches issued by this library so far (for benches). */
 uint64_t lpq_launch_count(void);
@@ -109,7 +114,9 @@ const char* lpq_last_cuda_error(void);
  *   index_base  : flat index of x[0] in the full tensor (RNG counter offset
  *                 for shards; 0 for a whole tensor)
  *   mode        : lpq_rounding; seed/call: RngStream seed and call id
- *   ws          : device workspace of >= lpq_workspace_size() bytes
+ *   ws          : device workspace of >= lpq_workspace_size() bytes; calls
+ *                 that may run concurrently (different streams) need their
+ *                 own workspaces
  *   d_status    : device uint32 the kernels OR error bits into (the caller
  *                 zeroes it; read it with lpq_status_fetch)
  *   stream      : cudaStream_t (NULL = legacy default stream) */
