@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
       if (j < hi) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
         if (Op::kBits && (M == kNearestEven || (M == kStochastic && IDX4))) {
-          // the variates' top words from the FMA-pipe hash (the bit-domain
-          // form is ALU-bound); the per-element forms take top >> 8.  (Testing
+          // the variates' top words (variate24_x4_top); the per-element
+          // forms take top >> 8.  (Testing
           // the range first and hashing per path inlines two hashes per
           // float4: C1 5095 -> 4874 GB/s, log-uniform 3506 -> 2720.)
           uint32_t tt[4] = {0u, 0u, 0u, 0u};

@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kGT)
   // for both ops: 953, for the multiply's only: 1064.)
   auto q = [&](float v, const FloatParams& p, uint32_t top) {
     if (M_ != kStochastic) return quant_float_bits<kNearestEven>(v, p, 0u);
-    return quant_float_bits_top(v, p, top, rm.one);
+    return quant_float_bits_top<true>(v, p, top, rm.one);
   };
   auto vars = [&](uint64_t key, uint64_t id, uint32_t (&top)[4]) {
     if (M_ != kStochastic) return;

@@ -272,16 +272,18 @@ LPQ_HD void variate24_x4(uint64_t key, uint64_t idx, uint32_t m32,
   const uint64_t w = (z0 & ~3ull) + 0x9E3779B97F4A7C15ull;
   const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
   const uint32_t kl = (uint32_t)key & 3u;
-  if (wlo > 0xFFFFFFFCu) {  // w + j_q may carry into the high word
+  if ((wlo & 0x3FFFFFFFu) > 0x3FFFFFFCu) {  // w + j_q may carry past bit 29
     for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m32) << (TOP ? 8 : 0);
     return;
   }
   const uint32_t h1 = whi ^ (whi >> 30);                   // shared
   const uint64_t hc = (uint64_t)(h1 * 0x1CE4E5B9u) << 32;  // shared hi*C1lo
+  // (z >> 30).lo = (zlo >> 30) | (zhi << 2): with no carry past bit 29,
+  // zlo >> 30 = wlo >> 30 for every lane, so the xor-shift word is shared
+  const uint32_t c30 = (wlo >> 30) | (whi << 2);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint32_t lo = wlo + (kl ^ (uint32_t)q);
-    lo ^= funnel_r<30>(lo, whi);
+    const uint32_t lo = (wlo + (kl ^ (uint32_t)q)) ^ c30;
     const uint64_t p = (uint64_t)lo * 0x1CE4E5B9u + hc;    // z *= C1
     uint32_t plo = (uint32_t)p;
     uint32_t phi = (uint32_t)(p >> 32) + lo * 0xBF58476Du;
@@ -332,33 +334,34 @@ LPQ_HD uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
 #endif
 }
 
-// variate24_x4 for the ALU-pipe-bound float kernels, returning the TOP
-// words of the last product (variate = top >> 8; the low 8 bits are hash
-// bits the caller ignores): the lane add as an IMAD against m.one and the
-// >> 27 xor-shift as IMAD.HI / IMAD against m.m32 (as variate24_zb), so
-// more of the hash issues on the FMA pipe; quant_float_bits_top folds the
-// >> 8 into its own shift.  Identical variates to variate24_z.
+// variate24_x4 for the elementwise float kernels, returning the TOP words of
+// the last product (variate = top >> 8; the low 8 bits are hash bits the
+// caller ignores; quant_float_bits_top folds the >> 8 into its own shift).
+// The xor-shifts are funnel shifts and the lane add a plain add; an
+// FMA-leaning form (lane add as IMAD, >> 27 as IMAD.HI / IMAD against m.m32)
+// measured slower once the >> 30 word was shared: C1 5030 -> 5300 GB/s with
+// these, log-uniform 3840 -> 3990.  Identical variates to variate24_z.
 LPQ_HD void variate24_x4_top(uint64_t key, uint64_t idx, const RngMul& m,
                              uint32_t out[4]) {
   const uint64_t z0 = key ^ idx;
   const uint64_t w = (z0 & ~3ull) + 0x9E3779B97F4A7C15ull;
   const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
   const uint32_t kl = (uint32_t)key & 3u;
-  if (wlo > 0xFFFFFFFCu) {  // w + j_q may carry into the high word
+  if ((wlo & 0x3FFFFFFFu) > 0x3FFFFFFCu) {  // w + j_q may carry past bit 29
     for (int q = 0; q < 4; ++q) out[q] = variate24_zb(z0 ^ (uint64_t)q, m.m32) << 8;
     return;
   }
   const uint32_t h1 = whi ^ (whi >> 30);                   // shared
   const uint64_t hc = (uint64_t)(h1 * 0x1CE4E5B9u) << 32;  // shared hi*C1lo
+  const uint32_t c30 = (wlo >> 30) | (whi << 2);           // shared (variate24_x4)
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint32_t lo = mad_lo(kl ^ (uint32_t)q, m.one, wlo);
-    lo ^= funnel_r<30>(lo, whi);
+    const uint32_t lo = (wlo + (kl ^ (uint32_t)q)) ^ c30;
     const uint64_t p = (uint64_t)lo * 0x1CE4E5B9u + hc;    // z *= C1
     uint32_t plo = (uint32_t)p;
     uint32_t phi = (uint32_t)(p >> 32) + lo * 0xBF58476Du;
-    const uint32_t slo = umulhi32(plo, m.m32) + phi * m.m32;  // (z >> 27).lo
-    const uint32_t shi = umulhi32(phi, m.m32);                // (z >> 27).hi
+    const uint32_t slo = funnel_r<27>(plo, phi);
+    const uint32_t shi = phi >> 27;
     plo ^= slo;
     phi ^= shi;
     out[q] = mulhi_sep(plo, 0x133111EBu) + plo * 0x94D049BBu + phi * 0x133111EBu;
@@ -706,20 +709,27 @@ LPQ_HD float quant_float_bits(float xc, const FloatParams& p, uint32_t v) {
 }
 
 // quant_float_bits<kStochastic> from the variate's top word (v = top >> 8,
-// the low 8 bits of top arbitrary): the sign spread as IMAD.HI.S32 and the
-// carry add as IMAD against the runtime one (FMA pipe), and
+// the low 8 bits of top arbitrary):
 // (top ^ (~neg & 0xFFFFFF00)) >> (8 + vshift) == (v ^ (~neg & 0xFFFFFF)) >> vshift.
+// FMA = true: the sign spread as IMAD.HI.S32 and the carry add as IMAD against
+// the runtime one, on the FMA pipe (the per-op GEMM's bits kernel, whose hash
+// holds the ALU pipe); false: SHF.R.S32 and IADD3 (the elementwise kernel:
+// C1 5304 -> 5369 GB/s).
+template <bool FMA = false>
 LPQ_HD float quant_float_bits_top(float xc, const FloatParams& p, uint32_t top,
                                   uint32_t one) {
   uint32_t b = f2u(xc);
+  int32_t neg;  // all ones iff x < 0
 #if defined(__CUDA_ARCH__)
-  int32_t neg;  // all ones iff x < 0: the high word of b * 1, signed
-  asm("mul.hi.s32 %0, %1, %2;" : "=r"(neg) : "r"((int32_t)b), "r"((int32_t)one));
+  if (FMA)  // the high word of b * 1, signed
+    asm("mul.hi.s32 %0, %1, %2;" : "=r"(neg) : "r"((int32_t)b), "r"((int32_t)one));
+  else
+    asm("shr.s32 %0, %1, 31;" : "=r"(neg) : "r"((int32_t)b));
 #else
-  const int32_t neg = (int32_t)b >> 31;
+  neg = (int32_t)b >> 31;
 #endif
   const uint32_t r = (top ^ (~(uint32_t)neg & 0xFFFFFF00u)) >> p.vshift8;
-  b = mad_lo(r, one, b);
+  b = FMA ? mad_lo(r, one, b) : b + r;
   return u2f(b & ~p.rmask);
 }
 

@@ -3,6 +3,7 @@
 // TEST INFRASTRUCTURE ONLY: not part of the product library; exists so the
 // exact source the sm_100a kernels inline can be swept over millions of
 // inputs on a machine without a GPU.
+#include <cstring>
 #include <math.h>
 #include <stdint.h>
 
@@ -127,7 +128,10 @@ void hm_quant_float_bits_top(const float* x, const uint32_t* top, float* y, int6
   const lpq::FloatParams p = lpq::make_float(exp_bits, man_bits);
   for (int64_t i = 0; i < n; ++i) {
     const float xc = fminf(fmaxf(x[i], -p.max_value), p.max_value);
-    y[i] = lpq::quant_float_bits_top(xc, p, top[i], 1u);
+    y[i] = lpq::quant_float_bits_top<false>(xc, p, top[i], 1u);
+    // the FMA-pipe form (the GEMM's) must agree bit for bit
+    const float yf = lpq::quant_float_bits_top<true>(xc, p, top[i], 1u);
+    if (memcmp(&yf, &y[i], 4) != 0) y[i] = __builtin_nanf("0x7ABCD");
   }
 }
 void hm_quant_float_bits(const float* x, const uint32_t* v, float* y, int64_t n,

@@ -98,6 +98,12 @@ def test_float4_variate_form_is_identical(hm):
     for d in range(0, 8):  # key ^ idx with (z & ~3) + C0 ending at 2^32 - 1 - d
         z = ((1 << 32) - 1 - d - (C0 & 0xFFFFFFFF)) & 0xFFFFFFFF | (0x12345 << 32)
         near.append((z & ~3 & (2**64 - 1), 0))
+    for top2 in range(4):  # ... and the shared >> 30 word (no carry past bit 29)
+        for d in range(0, 8):
+            wlo = (top2 << 30) | (0x3FFFFFFF - d)
+            z = ((wlo - (C0 & 0xFFFFFFFF)) & 0xFFFFFFFF) | (0xABCDE << 32)
+            near.append((z & ~3 & (2**64 - 1), 0))
+            near.append((0, z & ~3 & (2**64 - 1)))
     cases = [(0, 0), (0x5E41AB087439611E, 2**40), (2**64 - 1, 2**63), (3, 4), (6, 2**32 - 4)] + near
     for key, base in cases:
         n = 1 << 12
