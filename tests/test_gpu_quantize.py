@@ -776,3 +776,31 @@ def test_direct_host_path_byte_codes(q, case, mode):
         got = q.quantize_fused_at(host, spec, 2)
         got = got.numpy() if isinstance(got, torch.Tensor) else got
         assert same_bits(got, want), (case, mode)
+
+
+@pytest.mark.parametrize("n,base", [(300_001, 0), (1 << 20, 3), (262_144, 5),
+                                    (4_000_003, 1), (2_097_155, 2),
+                                    # sizes whose copy-pool parts used to drop a
+                                    # remainder (count / 16 a multiple of 64)
+                                    (1_048_577, 0), (4_194_305, 0)])
+@pytest.mark.parametrize("fmt_name", ["fixed84", "float52", "float43_wrapless", "float8_10"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_direct_host_path_ragged_and_index_base(q, n, base, fmt_name, mode):
+    """Pageable inputs take the direct host path up to 16 MB (staged copy in,
+    one-byte codes back for byte-coded formats, fp32 otherwise) and the
+    chunked stream beyond: ragged sizes, chunk boundaries that are not
+    multiples of 4 and index bases that are not multiples of 4 (the
+    variates' float4 grouping) must equal the device path bit for bit, and
+    the call counts one data pass."""
+    fmt = {"fixed84": q.FixedFormat(8, 4), "float52": q.FloatFormat(5, 2),
+           "float43_wrapless": q.FloatFormat(4, 3),
+           "float8_10": q.FloatFormat(8, 10)}[fmt_name]  # fp32 copy-back
+    rng = np.random.default_rng(n + base)
+    x = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-12, 12, n)).astype(np.float32)
+    x[:3] = [0.0, -0.0, 3.0]
+    spec = q.QuantSpec(fmt, q.RoundingMode(mode), 77)
+    want = q.quantize_fused_at(dev(x), spec, 5, index_base=base).cpu().numpy()
+    q.reset_pass_count()
+    got = q.quantize_fused_at(x, spec, 5, index_base=base)
+    assert q.pass_count() == 1
+    assert same_bits(got, want), (n, base, fmt_name, mode)
