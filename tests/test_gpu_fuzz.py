@@ -151,3 +151,46 @@ def test_fuzz_quant_gemm(q, oracle, seed):
 
 def _row_base_of(seed):
     return (seed * 37) % 100
+
+
+_HOST_SIZES = [1, 3, 4097, 65_535, 65_536, 65_537, 300_001, 1 << 20, (1 << 20) + 1,
+               (1 << 20) + 1025, 2_097_155, (1 << 22) - 1, 1 << 22, (1 << 22) + 1,
+               4_194_305, 5_000_003, 9_000_011]
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_fuzz_host_path_vs_device_path(chunk):
+    """The host entry point (staged copies, byte-coded or fp32 copy-back, the
+    direct path up to 16 MB and the chunked stream beyond, row-aligned chunks
+    for per-row block formats) against the device path on the same input:
+    random sizes around every threshold of the host runtime (the 256 KB
+    staging cut, the 16 MB direct cut, the copy pool's part rounding), random
+    formats, modes and index bases, pageable or pinned input.  Bit for bit."""
+    import paper_1910_04540_b200 as q
+    for seed in range(chunk * 12, (chunk + 1) * 12):
+        rng = np.random.default_rng(1000 + seed)
+        n = int(rng.choice(_HOST_SIZES)) + int(rng.integers(0, 3))
+        kind = int(rng.integers(0, 4))
+        if kind == 0:
+            f = q.FixedFormat(int(rng.integers(4, 13)), int(rng.integers(0, 8)), False,
+                              bool(rng.random() < 0.8))
+        elif kind == 1:
+            f = q.FloatFormat(int(rng.integers(2, 9)), int(rng.integers(0, 8)))
+        elif kind == 2:  # per-row blocks: row-aligned stream chunks
+            cols = int(rng.choice([64, 1000, 4096]))
+            n = max(cols, (n // cols) * cols)
+            f = q.BlockFloatFormat(int(rng.integers(4, 10)), 0)
+        else:
+            f = q.BlockFloatFormat(int(rng.integers(4, 10)))
+        shape = (n // cols, cols) if kind == 2 else (n,)
+        x = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-10, 10, n)).astype(np.float32)
+        x = x.reshape(shape)
+        mode = int(rng.integers(0, 4))
+        base = int(rng.choice([0, 1, 2, 3, 1 << 33]))
+        spec = q.QuantSpec(f, q.RoundingMode(mode), 0xF00D + seed)
+        want = q.quantize_fused_at(torch.from_numpy(x).cuda(), spec, 3,
+                                   index_base=base).cpu().numpy()
+        xin = x if rng.random() < 0.6 else torch.from_numpy(x.copy()).pin_memory()
+        got = q.quantize_fused_at(xin, spec, 3, index_base=base)
+        got = got.numpy() if isinstance(got, torch.Tensor) else got
+        assert np.array_equal(bits(got), bits(want)), (seed, n, f, mode, base, type(xin))
