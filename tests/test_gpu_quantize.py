@@ -804,3 +804,37 @@ def test_direct_host_path_ragged_and_index_base(q, n, base, fmt_name, mode):
     got = q.quantize_fused_at(x, spec, 5, index_base=base)
     assert q.pass_count() == 1
     assert same_bits(got, want), (n, base, fmt_name, mode)
+
+
+def test_host_path_concurrent_callers(q):
+    """Several host threads calling the host entry point at once (ctypes
+    releases the GIL): the per-device context lock and the shared copy pool
+    must keep every result bit-identical to the device path."""
+    import threading
+    cases = []
+    for i, (fmt, n) in enumerate([(q.FixedFormat(8, 4), 1 << 20), (q.FloatFormat(5, 2), 300_001),
+                                  (q.BlockFloatFormat(8), 1 << 21), (q.FloatFormat(8, 10), 5_000_003),
+                                  (q.FixedFormat(6, 2), 4_194_305), (q.BlockFloatFormat(6), 777)]):
+        rng = np.random.default_rng(40 + i)
+        x = (rng.uniform(-1, 1, n) * 4).astype(np.float32)
+        spec = q.QuantSpec(fmt, q.RoundingMode(i % 2), 90 + i)
+        want = q.quantize_fused_at(dev(x), spec, 1).cpu().numpy()
+        cases.append((x, spec, want))
+    errors = []
+
+    def worker(k):
+        try:
+            for r in range(3):
+                x, spec, want = cases[(k + r) % len(cases)]
+                got = q.quantize_fused_at(x, spec, 1)
+                if not same_bits(got, want):
+                    errors.append((k, r))
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
