@@ -141,14 +141,23 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
                   RngMul rm, uint32_t* __restrict__ status) {
+  // programmatic dependent launch: the next kernel of the stream may be
+  // scheduled once every CTA of this one has started (so only into the SM
+  // slots our last wave frees), and this one reads nothing before the
+  // previous kernel's writes are visible
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t n4 = (n - head) >> 2;
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
   float nf = 0.0f;
   const int64_t hi = n4;
   const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
-  for (int64_t i0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; i0 < hi;
-       i0 += step) {
+  // (hashing the first trip's variates before the wait, to overlap the
+  // previous kernel's tail, delays this kernel's loads: C1 5406 -> 5054-5113
+  // GB/s with two float4s' variates, 4346 with all seven)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t i_first = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
+  for (int64_t i0 = i_first; i0 < hi; i0 += step) {
     float4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -233,6 +242,32 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
     atomicOr(status, kStatusNonFinite);
 }
 
+// programmatic dependent launch for k_elementwise (LPQ_PDL=0 disables it):
+// C1 5350 -> 5390 GB/s, C1 nearest 6057 -> 6080-6170, C5 6243 -> 6293
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LPQ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// k_elementwise launches: with the programmatic-stream-serialization
+// attribute (see the kernel's griddepcontrol) when enabled
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ew_kernel(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 int64_t vector_head(const float* x, const float* y, int64_t n) {
   const uintptr_t ax = reinterpret_cast<uintptr_t>(x);
   const uintptr_t ay = reinterpret_cast<uintptr_t>(y);
@@ -278,33 +313,35 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
     // 5026 / 5121 vs 5057, within run-to-run noise or worse)
     const int64_t want = (work + (int64_t)kThreads * u - 1) / ((int64_t)kThreads * u);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
+    cudaError_t e;
     if (u == 5)
-      k_elementwise<M, Op, true, 5><<<grid, kThreads, 0, s>>>(x, y, n, head, base, key, op,
-                                                             rng_mul(), status);
+      e = launch_ew_kernel(k_elementwise<M, Op, true, 5>, grid, s, x, y, n, head, base, key, op,
+                           rng_mul(), status);
     else if (u == 7)
-      k_elementwise<M, Op, true, 7><<<grid, kThreads, 0, s>>>(x, y, n, head, base, key, op,
-                                                             rng_mul(), status);
+      e = launch_ew_kernel(k_elementwise<M, Op, true, 7>, grid, s, x, y, n, head, base, key, op,
+                           rng_mul(), status);
     else
-      k_elementwise<M, Op, true, 6><<<grid, kThreads, 0, s>>>(x, y, n, head, base, key, op,
-                                                             rng_mul(), status);
+      e = launch_ew_kernel(k_elementwise<M, Op, true, 6>, grid, s, x, y, n, head, base, key, op,
+                           rng_mul(), status);
     note_launch();
-    return cudaGetLastError();
+    return e;
   }
   const int unroll = small ? kUnrollSmall : kUnrollBig;
   const int64_t want = (work + (int64_t)kThreads * unroll - 1) /
                        ((int64_t)kThreads * unroll);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
+  cudaError_t e;
   if (small)
-    k_elementwise<M, Op, true, kUnrollSmall><<<grid, kThreads, 0, s>>>(
-        x, y, n, head, base, key, op, rng_mul(), status);
+    e = launch_ew_kernel(k_elementwise<M, Op, true, kUnrollSmall>, grid, s, x, y, n, head, base,
+                         key, op, rng_mul(), status);
   else if (idx4)
-    k_elementwise<M, Op, true, kUnrollBig><<<grid, kThreads, 0, s>>>(
-        x, y, n, head, base, key, op, rng_mul(), status);
+    e = launch_ew_kernel(k_elementwise<M, Op, true, kUnrollBig>, grid, s, x, y, n, head, base,
+                         key, op, rng_mul(), status);
   else
-    k_elementwise<M, Op, false, kUnrollBig><<<grid, kThreads, 0, s>>>(
-        x, y, n, head, base, key, op, rng_mul(), status);
+    e = launch_ew_kernel(k_elementwise<M, Op, false, kUnrollBig>, grid, s, x, y, n, head, base,
+                         key, op, rng_mul(), status);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 template <class Op>
