@@ -4,6 +4,7 @@
 
 general : k_qgemm_general (per-op GEMM float(5,2) stochastic, 2048^3, raw fp32 inputs)
 raw     : k_qgemm_bf16<raw> (per-op GEMM float(8,7) nearest, 4096^3, raw fp32 inputs)
+exact   : k_qgemm_bf16<exact> (C4: float(8,7)-exact operands, nearest, 4096^3)
 bits    : k_qgemm_bits (per-op GEMM float(8,7) stochastic, 2048^3, raw fp32 inputs)
 seg     : k_seg_reduce + k_seg_apply (block(8) whole tensor, 2^28)
 col     : k_col_reduce + k_col_apply (block(8) dim 1 on [2^22, 64])
@@ -39,10 +40,13 @@ elif what == "bits":
     c = torch.empty((n, n), device="cuda")
     for _ in range(reps):
         q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7), S, 3, out=c, sync=False)
-elif what == "raw":
+elif what in ("raw", "exact"):
     n = 4096
     a = q.random_uniform((n, n), 41, 0, -1.0, 1.0)
     b = q.random_uniform((n, n), 42, 0, -1.0, 1.0)
+    if what == "exact":  # operands pre-quantized to float(8,7) (BASELINE C4)
+        a = q.quantize_fused_at(a, q.QuantSpec(q.FloatFormat(8, 7), E, 1), 0)
+        b = q.quantize_fused_at(b, q.QuantSpec(q.FloatFormat(8, 7), E, 1), 0)
     c = torch.empty((n, n), device="cuda")
     for _ in range(reps):
         q.quant_gemm(a, b, q.FloatFormat(8, 7), q.FloatFormat(8, 7), E, out=c, sync=False)
