@@ -185,7 +185,10 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
           // full-mask vote for warps wholly inside the tensor, behind a
           // warp-uniform test, was slower: C1 4662, log-uniform 3612; so
           // was deferring the per-element float4s to a cold second loop to
-          // keep the hot code contiguous: C1 4568-4809 vs 5005-5011)
+          // keep the hot code contiguous: C1 4568-4809 vs 5005-5011; and the
+          // scaled form two elements at a time with FMUL2 / FFMA2.RM / FFMA2:
+          // ~7 instructions fewer per float4, log-uniform 3967 -> 3988-4005,
+          // C1 and nearest no better)
           if (__all_sync(__activemask(), op.in_range4(v[u]))) {
             o = op.template bits4<M>(v[u], tt, rm.one);
           } else {
