@@ -192,11 +192,12 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
           if (__all_sync(__activemask(), op.in_range4(v[u]))) {
             o = op.template bits4<M>(v[u], tt, rm.one);
           } else {
-            const int sh = M == kStochastic ? 8 : 0;
-            o.x = qelem_v<M>(op, v[u].x, tt[0] >> sh, nf);
-            o.y = qelem_v<M>(op, v[u].y, tt[1] >> sh, nf);
-            o.z = qelem_v<M>(op, v[u].z, tt[2] >> sh, nf);
-            o.w = qelem_v<M>(op, v[u].w, tt[3] >> sh, nf);
+            // v = top >> 8 as hi(top * 2^24): an IMAD.HI on the FMA pipe
+            const uint32_t m = M == kStochastic ? rm.m24 : 0u;
+            o.x = qelem_v<M>(op, v[u].x, umulhi32(tt[0], m), nf);
+            o.y = qelem_v<M>(op, v[u].y, umulhi32(tt[1], m), nf);
+            o.z = qelem_v<M>(op, v[u].z, umulhi32(tt[2], m), nf);
+            o.w = qelem_v<M>(op, v[u].w, umulhi32(tt[3], m), nf);
           }
           __stcs(y4 + j, o);
           continue;

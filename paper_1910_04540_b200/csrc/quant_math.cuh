@@ -558,6 +558,8 @@ struct FloatParams {
   uint32_t m_pos23;  // 2^23
   uint32_t sc_bits;  // (254 + man) << 23
   uint32_t inv_bits; // -man << 23 (mod 2^32)
+  uint32_t m_neg1;   // 2^32 - 1 and 1: runtime multipliers that keep the scaled
+  uint32_t m_one;    // form's exponent-field adds on the FMA pipe (mad_lo)
 };
 
 LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
@@ -587,6 +589,8 @@ LPQ_HD FloatParams make_float(int exp_bits, int man_bits) {
   p.m_pos23 = 1u << 23;
   p.sc_bits = (uint32_t)(254 + man_bits) << 23;
   p.inv_bits = 0u - ((uint32_t)man_bits << 23);
+  p.m_neg1 = 0xFFFFFFFFu;
+  p.m_one = 1u;
   p.bits_ok = man_bits <= 22 ? 1 : 0;
   p.rmask = man_bits <= 22 ? (1u << (23 - man_bits)) - 1u : 0u;
   p.rhalf = (p.rmask >> 1) + (man_bits == 0 ? 1u : 0u);
@@ -666,8 +670,10 @@ LPQ_HD float quant_float_scaled(float x, const FloatParams& p, uint32_t v) {
   // 2^(E - man) are one integer add each on it
   uint32_t eb = f2u(xc) & 0x7F800000u;
   eb = eb < ((uint32_t)p.ef_min << 23) ? ((uint32_t)p.ef_under << 23) : eb;
-  const float sc = u2f(p.sc_bits - eb);
-  const float inv = u2f(eb + p.inv_bits);
+  // sc_bits - eb and eb + inv_bits as IMADs (FMA pipe): the per-element
+  // path is ALU-bound (log-uniform C1: ALU 77 %)
+  const float sc = u2f(mad_lo(eb, p.m_neg1, p.sc_bits));
+  const float inv = u2f(mad_lo(eb, p.m_one, p.inv_bits));
   const float k = round_signed<M>(fmul(xc, sc), v);
   const float q = fma_rn(k, inv, 0.0f);
   return x == 0.0f ? x : q;
