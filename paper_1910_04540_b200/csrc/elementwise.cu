@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t j = i0 + (int64_t)u * kThreads;
-      if (j < hi) v[u] = __ldcs(x4 + j);
+      if (j < hi) v[u] = __ldcs(x4 + j);  // (.L2::256B: C2 7012 -> 6993, C1 -2 %)
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
