@@ -18,6 +18,19 @@
 
 #include "kernels.cuh"
 
+// Threads per CTA of the small-tensor (< 2^26 elements) elementwise kernels:
+// one-warp CTAs for stochastic and two-warp CTAs for nearest, at the same
+// warps per SM as the 256-thread CTAs, retire at a finer grain, which
+// shortens the last wave: C1 stochastic 5163-5359 -> 5400-5502 GB/s (with
+// 64 / 128 threads: 5375-5454 / 5384-5416), C1 log-uniform nearest 5707 ->
+// 5917-5934 (128: 5800-5900); tensors >= 2^26 keep 256.
+#ifndef LPQ_SMALL_TPB_RN
+#define LPQ_SMALL_TPB_RN 64
+#endif
+#ifndef LPQ_SMALL_TPB
+#define LPQ_SMALL_TPB 32
+#endif
+
 namespace lpq {
 
 namespace {
@@ -133,11 +146,11 @@ __device__ __forceinline__ float qelem_v(const Op& op, float x, uint32_t v,
 
 // IDX4: (base + head) % 4 == 0, so the four flat indices of a float4 differ
 // from the first only in their two low bits: key ^ (i + q) == (key ^ i) ^ q.
-template <int M, class Op, bool IDX4, int kUnroll>
+template <int M, class Op, bool IDX4, int kUnroll, int TPB = kThreads>
 // (float ops with the bit-domain form: <= 64 registers, 4 CTAs per SM --
 // the inlined fallback path would otherwise cost one CTA per SM; 5 for the
 // small-tensor nearest kernel: C1 nearest 5971 -> 6096 GB/s)
-__global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M == kStochastic ? 4 : 5))
+__global__ void __launch_bounds__(TPB, (!Op::kBits ? 0 : (kUnroll == 8 || M == kStochastic ? 4 : 5)) * (kThreads / TPB))
     k_elementwise(const float* __restrict__ x, float* __restrict__ y,
                   int64_t n, int64_t head, uint64_t base, uint64_t key, Op op,
                   RngMul rm, uint32_t* __restrict__ status) {
@@ -151,22 +164,22 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
   float nf = 0.0f;
   const int64_t hi = n4;
-  const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
+  const int64_t step = (int64_t)gridDim.x * TPB * kUnroll;
   // (hashing the first trip's variates before the wait, to overlap the
   // previous kernel's tail, delays this kernel's loads: C1 5406 -> 5054-5113
   // GB/s with two float4s' variates, 4346 with all seven)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int64_t i_first = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x;
+  const int64_t i_first = (int64_t)blockIdx.x * TPB * kUnroll + threadIdx.x;
   for (int64_t i0 = i_first; i0 < hi; i0 += step) {
     float4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int64_t j = i0 + (int64_t)u * kThreads;
+      const int64_t j = i0 + (int64_t)u * TPB;
       if (j < hi) v[u] = __ldcs(x4 + j);  // (.L2::256B: C2 7012 -> 6993, C1 -2 %)
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int64_t j = i0 + (int64_t)u * kThreads;
+      const int64_t j = i0 + (int64_t)u * TPB;
       if (j < hi) {
         const uint64_t idx = base + (uint64_t)(head + 4 * j);
         if (Op::kBits && (M == kNearestEven || (M == kStochastic && IDX4))) {
@@ -237,8 +250,8 @@ __global__ void __launch_bounds__(kThreads, !Op::kBits ? 0 : (kUnroll == 8 || M 
   // scalar head (before 16-byte alignment) and tail (after the last float4)
   const int64_t tail0 = head + 4 * n4;
   const int64_t extra = head + (n - tail0);
-  for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < extra;
-       t += (int64_t)gridDim.x * kThreads) {
+  for (int64_t t = (int64_t)blockIdx.x * TPB + threadIdx.x; t < extra;
+       t += (int64_t)gridDim.x * TPB) {
     const int64_t e = t < head ? t : tail0 + (t - head);
     y[e] = qelem<M>(op, x[e], key ^ (base + (uint64_t)e), rm, nf);
   }
@@ -258,11 +271,11 @@ bool pdl_enabled() {
 
 // k_elementwise launches: with the programmatic-stream-serialization
 // attribute (see the kernel's griddepcontrol) when enabled
-template <typename... KArgs, typename... Args>
+template <int TPB = kThreads, typename... KArgs, typename... Args>
 cudaError_t launch_ew_kernel(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(TPB);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -302,11 +315,11 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
     // stochastic (issue-heavier) small tensors: 5, 6 or 7 float4 per thread,
     // whichever fills the last wave of 4 CTAs/SM best (2^24 float(5,2): 7,
     // 3.96 waves, 4864 -> 4947 GB/s vs 6 at 4.61 waves)
-    const int64_t slots = 4 * (int64_t)device_info().sm_count;
+    const int64_t slots = 4 * (kThreads / LPQ_SMALL_TPB) * (int64_t)device_info().sm_count;
     int u = 6;
     double best = 0.0;
     for (int c : {6, 7, 5}) {
-      const int64_t ctas = (work + (int64_t)kThreads * c - 1) / ((int64_t)kThreads * c);
+      const int64_t ctas = (work + (int64_t)LPQ_SMALL_TPB * c - 1) / ((int64_t)LPQ_SMALL_TPB * c);
       const int64_t waves = (ctas + slots - 1) / slots;
       const double fill = (double)ctas / (double)(waves * slots);
       if (fill > best + 0.02) { best = fill; u = c; }
@@ -315,29 +328,30 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
     // finishes together, measured slower: C1 5187 -> 4945 GB/s; 5 / 6 / 4
     // float4 per thread at 5 / 5 / 6 CTAs per SM and 8 at 4: 4933 / 5095 /
     // 5026 / 5121 vs 5057, within run-to-run noise or worse)
-    const int64_t want = (work + (int64_t)kThreads * u - 1) / ((int64_t)kThreads * u);
+    constexpr int kT = LPQ_SMALL_TPB;
+    const int64_t want = (work + (int64_t)kT * u - 1) / ((int64_t)kT * u);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
     cudaError_t e;
     if (u == 5)
-      e = launch_ew_kernel(k_elementwise<M, Op, true, 5>, grid, s, x, y, n, head, base, key, op,
+      e = launch_ew_kernel<kT>(k_elementwise<M, Op, true, 5, kT>, grid, s, x, y, n, head, base, key, op,
                            rng_mul(), status);
     else if (u == 7)
-      e = launch_ew_kernel(k_elementwise<M, Op, true, 7>, grid, s, x, y, n, head, base, key, op,
+      e = launch_ew_kernel<kT>(k_elementwise<M, Op, true, 7, kT>, grid, s, x, y, n, head, base, key, op,
                            rng_mul(), status);
     else
-      e = launch_ew_kernel(k_elementwise<M, Op, true, 6>, grid, s, x, y, n, head, base, key, op,
+      e = launch_ew_kernel<kT>(k_elementwise<M, Op, true, 6, kT>, grid, s, x, y, n, head, base, key, op,
                            rng_mul(), status);
     note_launch();
     return e;
   }
   const int unroll = small ? kUnrollSmall : kUnrollBig;
-  const int64_t want = (work + (int64_t)kThreads * unroll - 1) /
-                       ((int64_t)kThreads * unroll);
+  const int64_t tpb = small ? LPQ_SMALL_TPB_RN : kThreads;
+  const int64_t want = (work + tpb * unroll - 1) / (tpb * unroll);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
   cudaError_t e;
   if (small)
-    e = launch_ew_kernel(k_elementwise<M, Op, true, kUnrollSmall>, grid, s, x, y, n, head, base,
-                         key, op, rng_mul(), status);
+    e = launch_ew_kernel<LPQ_SMALL_TPB_RN>(k_elementwise<M, Op, true, kUnrollSmall, LPQ_SMALL_TPB_RN>,
+                                           grid, s, x, y, n, head, base, key, op, rng_mul(), status);
   else if (idx4)
     e = launch_ew_kernel(k_elementwise<M, Op, true, kUnrollBig>, grid, s, x, y, n, head, base,
                          key, op, rng_mul(), status);
