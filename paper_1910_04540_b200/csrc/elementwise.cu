@@ -19,14 +19,15 @@
 #include "kernels.cuh"
 
 // Threads per CTA of the small-tensor (< 2^26 elements) elementwise kernels:
-// one-warp CTAs for stochastic and two-warp CTAs for nearest, at the same
+// one-warp CTAs for stochastic and four-warp CTAs for nearest, at the same
 // warps per SM as the 256-thread CTAs, retire at a finer grain, which
 // shortens the last wave: C1 stochastic 5163-5359 -> 5400-5502 GB/s (with
 // 64 / 128 threads: 5375-5454 / 5384-5416), C1 log-uniform nearest 5707 ->
-// 5917-5934 (128: 5800-5900); tensors >= 2^26 keep 256 (128 / 64 there:
-// C2 7021 -> 6937-6949 GB/s, float stochastic 2^30 +0.8 %).
+// 5800-5900 (64 threads: 5917-5934, but the C5 sweep's many small nearest
+// tensors 6268 -> 6250; 128: 6264); tensors >= 2^26 keep 256 (128 / 64
+// there: C2 7021 -> 6937-6949 GB/s, float stochastic 2^30 +0.8 %).
 #ifndef LPQ_SMALL_TPB_RN
-#define LPQ_SMALL_TPB_RN 64
+#define LPQ_SMALL_TPB_RN 128
 #endif
 #ifndef LPQ_SMALL_TPB
 #define LPQ_SMALL_TPB 32

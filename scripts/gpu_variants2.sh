@@ -1,6 +1,6 @@
 # A/B of library builds (lib/var/*.so) with an environment per variant
 mkdir -p gpurun_out/var
-for r in 1 2; do
+for r in $(seq ${REPS:-2}); do
 for v in $VARS; do
   cp paper_1910_04540_b200/lib/var/$v.so paper_1910_04540_b200/lib/liblpq.so
   for c in $CONFIGS; do
