@@ -329,7 +329,9 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
     // (a resident grid with equal contiguous shares per CTA, so every SM
     // finishes together, measured slower: C1 5187 -> 4945 GB/s; 5 / 6 / 4
     // float4 per thread at 5 / 5 / 6 CTAs per SM and 8 at 4: 4933 / 5095 /
-    // 5026 / 5121 vs 5057, within run-to-run noise or worse)
+    // 5026 / 5121 vs 5057, within run-to-run noise or worse; with one-warp
+    // CTAs, forcing 5 / 6 / 8 float4 per thread at 2^24: 4761 / 5090-5128 /
+    // 5434-5440 vs 5427-5455 for the 7 chosen here)
     constexpr int kT = LPQ_SMALL_TPB;
     const int64_t want = (work + (int64_t)kT * u - 1) / ((int64_t)kT * u);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7FFFFFFF));
