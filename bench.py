@@ -623,7 +623,7 @@ def run_gemm(args, rank, world, local_rank):
         "gpu_launches": q.launch_count() - l0,
         "roofline": {"bound": "fp32_cuda_core", "achieved": round(ach, 2),
                      "peak": round(peak_t, 2), "unit": "TFLOP/s",
-                     "frac": round(ach / peak_t, 4), "traffic": None,
+                     "frac": round(ach / peak_t, 4), "traffic": load_traffic(args.config),
                      "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz",
                      # the bf16 kernels' own bound: an HMUL2/HADD2 (or FMUL
                      # pair + HADD2) per 64 MACs per warp holds the FMA pipe
@@ -711,7 +711,7 @@ def run_matmul_q(args, rank, world, local_rank):
         "gpu_launches": q.launch_count() - l0,
         "roofline": {"bound": "fp64 tensor (DMMA)", "achieved": round(ach, 2), "unit": "TFLOP/s",
                      "peak": FP64_DMMA_PEAK, "frac": round(ach / FP64_DMMA_PEAK, 4),
-                     "traffic": None,
+                     "traffic": load_traffic("c4ref"),
                      "peak_source": "measured in-repo: register-resident DMMA m8n8k4 loop on "
                                     "this B200 (scripts/dmma_rate.cu; DFMA: 33.4); "
                                     "MEASURED_PEAKS.json has no FP64 figure"},
