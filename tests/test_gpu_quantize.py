@@ -838,3 +838,55 @@ def test_host_path_concurrent_callers(q):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("n", [1 << 20, (1 << 26) + 12, 300_001])
+def test_dependent_launch_chains(q, n):
+    """Back-to-back quantizations on one stream where each reads the previous
+    one's output (and in place), launched under programmatic dependent
+    launch with no host synchronisation between them: every result must
+    equal the same chain run with a full synchronisation after each call
+    (griddepcontrol.wait orders each kernel's loads after its predecessor)."""
+    x = q.random_uniform((n,), 11, 0, -6.0, 6.0)
+    specs = [q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode.Stochastic, 3),
+             q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.NearestEven, 4),
+             q.QuantSpec(q.FloatFormat(4, 3), q.RoundingMode.Stochastic, 5),
+             q.QuantSpec(q.FixedFormat(6, 2), q.RoundingMode.Stochastic, 6)]
+    want = []
+    cur = x
+    for i, sp in enumerate(specs):
+        cur = q.quantize_fused_at(cur, sp, i)
+        torch.cuda.synchronize()
+        want.append(cur.clone())
+    # the same chain, no synchronisation, alternating fresh and in-place outputs
+    a = torch.empty_like(x)
+    b = torch.empty_like(x)
+    q.quantize_fused_at(x, specs[0], 0, out=a, sync=False)
+    q.quantize_fused_at(a, specs[1], 1, out=b, sync=False)
+    q.quantize_fused_at(b, specs[2], 2, out=b, sync=False)   # in place
+    q.quantize_fused_at(b, specs[3], 3, out=a, sync=False)
+    q.fetch_status()
+    torch.cuda.synchronize()
+    assert same_bits(a, want[3].cpu().numpy())
+
+
+def test_dependent_launch_reads_the_predecessors_last_wave(q):
+    """The sharpest case for programmatic dependent launch: the second kernel
+    reads the LAST slice of the first one's output (which the first kernel's
+    last wave writes while the second kernel's CTAs are already being
+    scheduled).  Without griddepcontrol.wait this reads stale memory."""
+    n, m = (1 << 26) + 4096, 1 << 20
+    x = q.random_uniform((n,), 13, 0, -6.0, 6.0)
+    s1 = q.QuantSpec(q.FixedFormat(8, 4), q.RoundingMode.NearestEven, 1)
+    s2 = q.QuantSpec(q.FloatFormat(5, 2), q.RoundingMode.Stochastic, 2)
+    want = q.quantize_fused_at(q.quantize_fused_at(x, s1, 0)[n - m:].contiguous(), s2, 0)
+    torch.cuda.synchronize()
+    for rep in range(20):
+        a = torch.full_like(x, 1e3)            # stale contents that quantize differently
+        b = torch.empty((m,), device="cuda")
+        torch.cuda.synchronize()
+        q.quantize_fused_at(x, s1, 0, out=a, sync=False)
+        q.quantize_fused_at(a[n - m:], s2, 0, out=b, sync=False)
+        q.fetch_status()
+        torch.cuda.synchronize()
+        assert same_bits(b, want.cpu().numpy()), rep
