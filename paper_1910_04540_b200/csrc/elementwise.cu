@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(TPB, (!Op::kBits ? 0 : (kUnroll == 8 || M == k
   // scheduled once every CTA of this one has started (so only into the SM
   // slots our last wave frees), and this one reads nothing before the
   // previous kernel's writes are visible
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_trigger();
   const int64_t n4 = (n - head) >> 2;
   const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
   float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(TPB, (!Op::kBits ? 0 : (kUnroll == 8 || M == k
   // (hashing the first trip's variates before the wait, to overlap the
   // previous kernel's tail, delays this kernel's loads: C1 5406 -> 5054-5113
   // GB/s with two float4s' variates, 4346 with all seven)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_wait();
   const int64_t i_first = (int64_t)blockIdx.x * TPB * kUnroll + threadIdx.x;
   for (int64_t i0 = i_first; i0 < hi; i0 += step) {
     float4 v[kUnroll];
@@ -261,30 +261,12 @@ __global__ void __launch_bounds__(TPB, (!Op::kBits ? 0 : (kUnroll == 8 || M == k
     atomicOr(status, kStatusNonFinite);
 }
 
-// programmatic dependent launch for k_elementwise (LPQ_PDL=0 disables it):
-// C1 5350 -> 5390 GB/s, C1 nearest 6057 -> 6080-6170, C5 6243 -> 6293
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("LPQ_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// k_elementwise launches: with the programmatic-stream-serialization
-// attribute (see the kernel's griddepcontrol) when enabled
+// k_elementwise launches under programmatic dependent launch (kernels.cuh
+// launch_pdl): C1 5350 -> 5390 GB/s, C1 nearest 6057 -> 6080-6170, C5 6243
+// -> 6293
 template <int TPB = kThreads, typename... KArgs, typename... Args>
 cudaError_t launch_ew_kernel(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(TPB);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k, args...);
+  return launch_pdl(k, dim3((unsigned)grid), dim3(TPB), s, args...);
 }
 
 int64_t vector_head(const float* x, const float* y, int64_t n) {
@@ -525,6 +507,14 @@ cudaError_t launch_encode_block8(const float* q, uint8_t* c, const BlockGeom& g,
                                                       wl, not_exact);
   note_launch();
   return cudaGetLastError();
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LPQ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace lpq

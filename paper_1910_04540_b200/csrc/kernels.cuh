@@ -105,6 +105,34 @@ cudaError_t launch_encode_block8(const float* q, uint8_t* c, const BlockGeom& g,
                                  const uint32_t* maxima, int wl, uint32_t* not_exact,
                                  cudaStream_t s);
 
+// ---- programmatic dependent launch (LPQ_PDL=0 disables it) -----------------
+// A kernel launched by launch_pdl may be scheduled while the previous kernel
+// of the stream drains; it calls pdl_trigger() first (so its own successor
+// can only be scheduled once every CTA of this grid has started) and
+// pdl_wait() before its first global memory access (which returns once the
+// predecessor has completed and its writes are visible).  Without the launch
+// attribute both are no-ops.  Used by k_elementwise; the block-row and
+// grouped kernels under it measured no different (C5 6284-6285 either way).
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 cudaError_t launch_uniform(float* y, int64_t n, uint64_t base, uint64_t key,
                            float lo, float hi, cudaStream_t s);
 cudaError_t launch_variates(float* y, int64_t n, uint64_t base, uint64_t key,
