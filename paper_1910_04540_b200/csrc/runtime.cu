@@ -577,15 +577,20 @@ lpq_status stream_quantize(HostCtx* c, const float* x, float* y, int64_t n,
                            int64_t unit, bool rows, uint64_t index_base,
                            const lpq_format* f, int mode, uint64_t seed,
                            uint64_t call) {
-  // at least ~16 chunks when the tensor allows (chunks of 1 MB .. 64 MB), so
-  // mid-size tensors overlap copy-in, kernel, copy-out and decode too: the
-  // 64 MB C1 tensor's e2e 64 -> 84-88 GB/s with 16 chunks of 4 MB instead of
-  // 4 of 16 MB (8: 75-76, 32: 72-73; the 1 GB tensors keep 64 MB chunks)
+  // Chunks of 1 MB .. 64 MB.  Into page-locked output memory (the decode
+  // runs at memory speed) at least ~16 chunks, so mid-size tensors overlap
+  // copy-in, kernel, copy-out and decode: the 64 MB C1 tensor's e2e 64 ->
+  // 84-88 GB/s with 16 chunks of 4 MB instead of 4 of 16 MB (8: 75-76, 32:
+  // 72-73).  Into pageable memory not yet touched, the decode also takes the
+  // page faults and smaller chunks stall the three-deep pipeline behind it
+  // (32 MB: 2.47 / 2.66 / 4.28 ms with 4 / 8 / 16 chunks), so ~4 there.  1 GB
+  // tensors keep 64 MB chunks either way.
+  const bool pin_x = is_pinned(x), pin_y = is_pinned(y);
+  const int64_t min_chunks = pin_y ? 16 : 4;
   const int64_t target = std::min<int64_t>(
-      kChunkElems, std::max<int64_t>(int64_t(1) << 18, (n + 15) / 16));
+      kChunkElems, std::max<int64_t>(int64_t(1) << 18, (n + min_chunks - 1) / min_chunks));
   const int64_t chunk = std::max<int64_t>(1, target / unit) * unit;
   LPQ_TRY(c->ensure_chunks(std::max<int64_t>(chunk, c->chunk_cap)));
-  const bool pin_x = is_pinned(x), pin_y = is_pinned(y);
   const int64_t nchunks = (n + chunk - 1) / chunk;
   lpq_format fr = *f;
   if (rows) fr.block_dim = 0;
