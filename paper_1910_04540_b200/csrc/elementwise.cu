@@ -286,6 +286,9 @@ cudaError_t launch_ew(const float* x, float* y, int64_t n, uint64_t base,
   const int64_t n4 = (n - head) >> 2;
   const int64_t work = std::max<int64_t>(n4, n - 4 * n4);
   const bool idx4 = ((base + (uint64_t)head) & 3u) == 0;
+  // (A TMA variant -- one cp.async.bulk of a 32 KB tile into shared memory
+  // per CTA, quantize there, one bulk store -- measured slower on C2: 6880
+  // GB/s at 6 CTAs/SM, 6695 with 16 KB tiles at 8, vs 6984-7022.)
   // One trip per thread over the whole tensor (not a persistent grid): CTAs
   // retire and launch in address order, which keeps the DRAM pages in use
   // compact.  Measured on B200 (scripts/ew_variants.cu, 2^30 elements):
